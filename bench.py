@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark: RASTER contraction + agglomeration on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 4] [--order gen|shuffled] [--quick]
+
+One step = cluster_sequential over the whole workload: K1 contraction, K2
+compaction, K3 connected components + mu filter + canonical ids (results
+device-resident). Headline workload: BASELINE config 4 (500M float64 points,
+8 GB, 1,000,000 Gaussian clusters x 500, sigma 5e-4, p=3, tau=4, mu=4) in
+generation order; inputs (8 GB) exceed the 126 MB L2, so no flush is needed
+between steps.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "points/sec clustered at 1 B200 (contraction+agglomeration); % of HBM roofline"
+BYTES_PER_POINT = 16  # algorithmic: read (x, y) float64 once
+WORKLOADS = {
+    1: "config1: 1M pts, 1,000 Gaussian clusters x 1,000 (sigma 0.005), p=2 tau=5 mu=4",
+    2: "config2: 10M pts, 10,000 clusters x 900 (sigma 0.005) + 1M uniform noise, p=2 tau=5 mu=4",
+    3: "config3: 100M pts, 100,000 clusters x 1,000 (sigma 5e-4), p=3 tau=5 mu=4",
+    4: "config4: 500M pts (8 GB), 1,000,000 Gaussian clusters x 500 (sigma 5e-4), p=3 tau=4 mu=4",
+    5: "config5: 200M pts, 100M blob (sigma 1e-4) + 1,000 walks x 20,000 steps x 3 + 40M noise, p=3 tau=3 mu=4",
+}
+
+
+def measured_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        v = float(json.loads(p.read_text())["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def reference_arm(args) -> None:
+    """The reference's own CPU implementation (oracle/_ref = the reference
+    compiled from its headers) on this host's cores, on a bounded sample of
+    the same workload."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import pyoracle as O
+    from paper_1907_03620_b200 import datagen as D
+
+    if O.ref() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libraster_ref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    workers = args.ref_workers if args.ref_workers is not None else cores
+    s = D.spec(args.config)
+    per = s.points_per_cluster
+    sample_pts = min(args.ref_sample, D.count(s))
+    full = D.count(s)
+    # bounded sample = the first clusters of the workload (generation order)
+    s.n_clusters = max(1, sample_pts // max(per, 1)) if per else s.n_clusters
+    pts = D.generate(s, shuffle_seed=(11 if args.order == "shuffled" else None))
+    gp = D.params(args.config)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, tp, tc, nc = O.ref_time(pts.ctypes.data, pts.shape[0], gp, workers)
+        if i >= args.warmup:
+            times.append(t)
+    n = pts.shape[0]
+    med = statistics.median(times)
+    value = n / med
+    kind = "reference"
+    sample = (f"first {n:,} points ({s.n_clusters:,} clusters) of {WORKLOADS[args.config].split(':')[0]} "
+              f"({full:,} points), {args.order} order; raster::cluster_"
+              f"{'parallel' if workers else 'sequential'} count mode")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "order": args.order,
+                   "parallelism": f"cpu x{max(workers, 1)} threads"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": max(workers, 1),
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def cpu_baseline_sequential(pts_host, gp, n_sample: int) -> dict:
+    """Reference cluster_sequential (1 core) on a bounded sample."""
+    from oracle import pyoracle as O
+
+    if O.ref() is None:
+        t0 = time.perf_counter()
+        O.port_cluster(pts_host[:n_sample], gp)
+        t = time.perf_counter() - t0
+        kind = "port"
+    else:
+        t, _, _, _ = O.ref_time(pts_host.ctypes.data, n_sample, gp, 0)
+        kind = "reference"
+    return {"value": n_sample / t, "unit": "points/s", "cores": 1, "kind": kind,
+            "sample": f"first {n_sample:,} points of the workload (generation order), "
+                      f"raster::cluster_sequential count mode, 1 thread"}
+
+
+def ours(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_1907_03620_b200 import datagen as D
+    from paper_1907_03620_b200.raster import Pipeline
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    cfg = args.config
+    s = D.spec(cfg)
+    if world > 1:  # weak scaling: each rank clusters its own seeded shard
+        s.seed = s.seed + 7919 * rank
+    n = D.count(s)
+    gp = D.params(cfg)
+
+    host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+    t0 = time.perf_counter()
+    D.generate_into(s, host.data_ptr())
+    if args.order == "shuffled":
+        host.numpy()[:] = D.shuffle(host.numpy(), 11)
+    t_gen = time.perf_counter() - t0
+    dev = host.to(f"cuda:{local}", non_blocking=False)
+    stream = torch.cuda.current_stream()
+    pl = Pipeline(gp, device=local)
+    pl.set_stream(stream.cuda_stream)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pl.run(dev)
+    barrier()
+    launches0 = pl.launches()
+    ms_contract = []
+    st = None
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = pl.run(dev)
+            ms_contract.append(st.ms_contract)
+        e1.record(stream)
+        barrier()
+    launches = pl.launches() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n * world / (ms_step / 1e3)
+
+    # e2e: through the public API from pinned host memory, reading the
+    # canonical result (sorted significant tiles + counts + cluster ids) back.
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    S = st.n_significant
+    tx = np.empty(S, np.int64)
+    ty = np.empty(S, np.int64)
+    cnt = np.empty(S, np.uint64)
+    cid = np.empty(S, np.int64)
+    from paper_1907_03620_b200 import _native as N
+
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        pl.run(host)
+        pl.ctx.check(pl.ctx.lib.rg_get_significant(pl.ctx.h, tx.ctypes.data, ty.ctypes.data,
+                                                   cnt.ctypes.data, cid.ctypes.data, S,
+                                                   N.RG_MEM_HOST))
+    f1.record(stream)
+    barrier()
+    ms_e2e = f0.elapsed_time(f1) / e2e_steps
+    if dist:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = n * world / (ms_e2e / 1e3)
+
+    extra = {}
+    if not args.quick and rank == 0:
+        # point-retaining variant: + per-point int32 labels (20 B/pt algorithmic)
+        labels = torch.empty(n, dtype=torch.int32, device=dev.device)
+        pl.run(dev)
+        pl.label_points(dev, labels)
+        torch.cuda.synchronize()
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for _ in range(args.steps):
+            pl.run(dev)
+            pl.label_points(dev, labels)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        ms_l = l0.elapsed_time(l1) / args.steps
+        peak, _ = measured_peak_gbs()
+        extra["labelled"] = {"points_per_s": n / (ms_l / 1e3), "ms_per_step": ms_l,
+                             "roofline_frac_20B": (20 * n / (ms_l / 1e3)) / (peak * 1e9)}
+        del labels
+
+    peak, peak_src = measured_peak_gbs()
+    k1_ms = statistics.mean(ms_contract)
+    achieved = BYTES_PER_POINT * n / (k1_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, include/raster_datagen.h)",
+        "config": {"workload": WORKLOADS[cfg], "order": args.order, "points": n * world,
+                   "l2": "inputs 8 GB >> 126 MB L2 each step (no flush needed)" if n >= 100_000_000
+                   else "inputs smaller than L2: not flushed",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} ranks, independent shards (no cross-rank merge)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "K1 contraction (k_contract), 16 B/point, ms from CUDA events on the launch stream",
+                     "peak_source": peak_src,
+                     "end_to_end_frac": (BYTES_PER_POINT * n / (ms_step / 1e3) / 1e9) / peak},
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 32 * S},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "phases_ms": {"contract": st.ms_contract, "prune": st.ms_prune,
+                      "agglomerate": st.ms_agglomerate},
+        "sizes": {"distinct_tiles": st.peak_accumulator_entries, "significant": S,
+                  "clusters": st.n_clusters, "table_capacity": st.table_capacity,
+                  "grows_total": st.table_grows},
+        "gen_seconds": t_gen,
+    }
+    if extra:
+        line["extra"] = extra
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_sample = min(n, args.cpu_sample)
+        line["cpu_baseline"] = cpu_baseline_sequential(host.numpy(), gp, n_sample)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--order", choices=["gen", "shuffled"], default="gen")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=20_000_000)
+    ap.add_argument("--ref-sample", type=int, default=20_000_000)
+    ap.add_argument("--ref-workers", type=int, default=None)
+    ap.add_argument("--quick", action="store_true", help="skip the labelled-variant extra")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

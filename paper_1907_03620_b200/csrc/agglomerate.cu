@@ -1,0 +1,240 @@
+// agglomerate.cu — K3: connected components over the significant tiles, the
+// mu size filter and canonical relabelling, for sm_100a.
+//
+// Replaces connected_components (agglomerate.hpp:124-170: flat index +
+// explicit-stack DFS with one hash probe per neighbour offset), the size
+// filter in agglomerate (:196-201) and finalize_clusters (:175-191).
+//
+// Algorithm (all O(S), no full sort):
+//   1. union   — one thread per significant tile probes the forward half of
+//                the delta-ball (the ball is symmetric, so every adjacent
+//                pair is seen exactly once) in the HBM hash table, whose
+//                value word already holds SIG_BIT|index after K2, and unites
+//                the two components. Union-find hooks the larger root under
+//                the smaller (ECL-CC style CAS loop, path halving in find),
+//                which keeps parent[x] <= x and converges in O(S α) work even
+//                for config 5's 10^4-tile chains, where label propagation
+//                would need diameter-many rounds.
+//   2. compress — parent[i] = root(i).
+//   3. reduce  — per root: tile count, point count and the smallest packed
+//                key (= the cluster's lexicographically smallest tile, the
+//                sort key of finalize_clusters :186-189).
+//   4. select  — roots with size >= mu are appended as (min_key, root).
+//   5. order   — the C kept roots (C <= S) are radix-sorted by min_key; the
+//                rank is the canonical cluster id (:189-190).
+//   6. label   — every tile gets the id of its root (or -1).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rg {
+
+__device__ __forceinline__ u32 ld_parent(const u32* p) {
+    u32 v;
+    asm volatile("ld.global.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ u32 uf_find(u32* parent, u32 v) {
+    u32 par = ld_parent(parent + v);
+    if (par != v) {
+        u32 prev = v, next;
+        while (par > (next = ld_parent(parent + par))) {
+            parent[prev] = next;  // path halving; monotone, benign race
+            prev = par;
+            par = next;
+        }
+    }
+    return par;
+}
+
+__device__ __forceinline__ void uf_unite(u32* parent, u32 a, u32 b) {
+    u32 ra = uf_find(parent, a);
+    u32 rb = uf_find(parent, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 t = ra;
+            ra = rb;
+            rb = t;
+        }
+        // hook ra (larger) under rb (smaller)
+        const u32 old = atomicCAS(parent + ra, ra, rb);
+        if (old == ra) return;
+        ra = old;  // ra was hooked meanwhile: continue from its new parent
+    }
+}
+
+struct Offsets {
+    const int2* d;  // forward half of the delta-ball
+    int n;
+};
+
+__global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bits_y,
+                        u32 bits_x, Offsets off, u32* parent) {
+    const u64 n_sig = *n_sig_p;
+    const long long ymask = (1ll << bits_y) - 1;
+    const long long xlim = 1ll << bits_x, ylim = 1ll << bits_y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 key = sig_key[i];
+        const long long kx = (long long)(key >> bits_y);
+        const long long ky = (long long)key & ymask;
+        for (int o = 0; o < off.n; ++o) {
+            const int2 d = off.d[o];
+            const long long nx = kx + d.x, ny = ky + d.y;
+            if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) continue;
+            const u64 nkey = ((u64)nx << bits_y) | (u64)ny;
+            const u64 v = table_find(t, nkey);
+            if (v != kEmpty && (v & kSigBit)) uf_unite(parent, (u32)i, (u32)(v & ~kSigBit));
+        }
+    }
+}
+
+__global__ void k_compress(u32* parent, const u64* n_sig_p) {
+    const u64 n_sig = *n_sig_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+         i += (u64)gridDim.x * blockDim.x)
+        parent[i] = uf_find(parent, (u32)i);
+}
+
+// Per-root reductions. size/points start at 0, min_key at kEmpty.
+__global__ void k_root_reduce(const u32* parent, const u64* sig_key, const u64* sig_cnt,
+                              const u64* n_sig_p, u32* size, u64* npts, u64* min_key) {
+    const u64 n_sig = *n_sig_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 r = parent[i];
+        atomicAdd(size + r, 1u);
+        atomicAdd(npts + r, sig_cnt ? sig_cnt[i] : 0ull);
+        atomicMin(min_key + r, sig_key[i]);
+    }
+}
+
+// Roots with size >= mu -> (min_key, root) pairs; counts components.
+__global__ void k_select_roots(const u32* parent, const u32* size, const u64* min_key,
+                               const u64* n_sig_p, u64 mu, u64* out_key, u32* out_root,
+                               Counters* ctr) {
+    const u64 n_sig = *n_sig_p;
+    const int lane = threadIdx.x & 31;
+    for (u64 base = blockIdx.x * (u64)blockDim.x; base < n_sig;
+         base += (u64)gridDim.x * blockDim.x) {
+        const u64 i = base + threadIdx.x;
+        const bool root = i < n_sig && parent[i] == (u32)i;
+        const bool keep = root && size[i] >= mu;
+        const u32 rmask = __ballot_sync(kFull, root);
+        const u32 kmask = __ballot_sync(kFull, keep);
+        u64 at = 0;
+        if (lane == 0) {
+            if (rmask) atomicAdd(&ctr->n_roots, (u64)__popc(rmask));
+            if (kmask) at = atomicAdd(&ctr->n_kept, (u64)__popc(kmask));
+        }
+        at = __shfl_sync(kFull, at, 0);
+        if (keep) {
+            const u64 pos = at + __popc(kmask & ((1u << lane) - 1));
+            out_key[pos] = min_key[i];
+            out_root[pos] = (u32)i;
+        }
+    }
+}
+
+__global__ void k_assign_ids(const u32* root_sorted, const u64* n_kept_p, int* root_cid) {
+    const u64 n = *n_kept_p;
+    for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < n;
+         k += (u64)gridDim.x * blockDim.x)
+        root_cid[root_sorted[k]] = (int)k;
+}
+
+__global__ void k_label_tiles(const u32* parent, const int* root_cid, const u64* n_sig_p,
+                              int* tile_cid) {
+    const u64 n_sig = *n_sig_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+         i += (u64)gridDim.x * blockDim.x)
+        tile_cid[i] = root_cid[parent[i]];
+}
+
+// Load path (agglomerate(SignificantTiles) with caller tiles): pack and insert
+// every tile as significant with its dense index.
+__global__ void k_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
+                             long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                             u64* sig_cnt, u32* parent) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 key = ((u64)(tx[i] - ox) << bits_y) | (u64)(ty[i] - oy);
+        sig_key[i] = key;
+        sig_cnt[i] = cnt ? cnt[i] : 0;
+        parent[i] = (u32)i;
+        u64 s = slot_of(key, t.shift);
+        while (true) {
+            const u64 old = atomicCAS(&t.slots[s].key, kEmpty, key);
+            if (old == kEmpty || old == key) {
+                t.slots[s].count = kSigBit | i;
+                break;
+            }
+            s = (s + 1) & t.mask;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- launchers
+
+static int grid_for(u64 n, int n_sm, int per_sm = 8) {
+    const u64 want = (n + 255) / 256;
+    const u64 cap = (u64)n_sm * per_sm;
+    return (int)(want == 0 ? 1 : (want < cap ? want : cap));
+}
+
+cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
+    const int gs = grid_for(A.n_sig, A.n_sm, 16);
+    Offsets off{A.offsets, A.n_offsets};
+    cudaMemsetAsync(A.size, 0, A.n_sig * sizeof(u32), st);
+    cudaMemsetAsync(A.npts, 0, A.n_sig * sizeof(u64), st);
+    cudaMemsetAsync(A.min_key, 0xff, A.n_sig * sizeof(u64), st);
+    cudaMemsetAsync(A.root_cid, 0xff, A.n_sig * sizeof(int), st);
+    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent);
+    k_compress<<<gs, 256, 0, st>>>(A.parent, A.n_sig_dev);
+    k_root_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size, A.npts,
+                                      A.min_key);
+    k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,
+                                       A.root_key, A.root_idx, A.ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_order_and_label(const AggLaunch& A, u64 n_kept, cudaStream_t st) {
+    if (n_kept > 0) {
+        size_t bytes = A.sort_temp_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(
+            A.sort_temp, bytes, A.root_key, A.root_key_sorted, A.root_idx, A.root_idx_sorted,
+            (int)n_kept, 0, (int)(A.bits_x + A.bits_y), st);
+        if (e != cudaSuccess) return e;
+        k_assign_ids<<<grid_for(n_kept, A.n_sm), 256, 0, st>>>(A.root_idx_sorted,
+                                                                &A.ctr->n_kept, A.root_cid);
+    }
+    k_label_tiles<<<grid_for(A.n_sig, A.n_sm, 16), 256, 0, st>>>(A.parent, A.root_cid,
+                                                                 A.n_sig_dev, A.tile_cid);
+    return cudaGetLastError();
+}
+
+size_t sort_pairs_temp_bytes(u64 n, int bits) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs((void*)nullptr, bytes, (const u64*)nullptr, (u64*)nullptr,
+                                    (const u32*)nullptr, (u32*)nullptr, (int)n, 0, bits);
+    return bytes;
+}
+
+cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_out,
+                       const u32* v_in, u32* v_out, u64 n, int bits, cudaStream_t st) {
+    size_t bytes = temp_bytes;
+    return cub::DeviceRadixSort::SortPairs(temp, bytes, k_in, k_out, v_in, v_out, (int)n, 0,
+                                           bits, st);
+}
+
+cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
+                              long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                              u64* sig_cnt, u32* parent, int n_sm, cudaStream_t st) {
+    k_load_tiles<<<grid_for(n, n_sm), 256, 0, st>>>(tx, ty, cnt, n, ox, oy, bits_y, t, sig_key,
+                                                     sig_cnt, parent);
+    return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -1,0 +1,1365 @@
+// api.cu — the C-ABI (include/raster_gpu.h): context lifetime, the
+// accumulator state machine of TileAccumulator (accumulator.hpp:109-214), the
+// composed pipeline of cluster_sequential (pipeline.hpp:92-126), host<->device
+// staging, and small utility kernels. No CPU fallback anywhere: every
+// computational entry point runs on the device or fails.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/raster_gpu.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+constexpr double kMaxLoad = 0.7;  // TileCounts grows at 70% load (accumulator.hpp:34)
+constexpr u64 kStagePoints = 1ull << 24;  // 256 MB per staging buffer
+
+u64 next_pow2(u64 v) {
+    u64 p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+u32 bits_for(double count) {  // smallest b with 2^b >= count, at least 1
+    u32 b = 1;
+    while (b < 64 && std::ldexp(1.0, (int)b) < count) ++b;
+    return b;
+}
+
+u32 log2u(u64 v) {
+    u32 b = 0;
+    while ((1ull << b) < v) ++b;
+    return b;
+}
+
+// Forward half of neighbor_offsets (agglomerate.hpp:38-50): the delta-ball of
+// the metric minus the centre, restricted to dx > 0 or (dx == 0 and dy > 0).
+std::vector<int2> forward_offsets(const rg_params& p) {
+    std::vector<int2> out;
+    const int d = p.distance;
+    for (int dx = -d; dx <= d; ++dx)
+        for (int dy = -d; dy <= d; ++dy) {
+            if (dx == 0 && dy == 0) continue;
+            if (p.metric == RG_METRIC_MANHATTAN && std::abs(dx) + std::abs(dy) > d) continue;
+            if (dx > 0 || (dx == 0 && dy > 0)) out.push_back(make_int2(dx, dy));
+        }
+    return out;
+}
+
+struct DevGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DevGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) {
+            changed = cudaSetDevice(d) == cudaSuccess;
+        }
+    }
+    ~DevGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
+__global__ void k_iota(u32* out, u64 n) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        out[i] = (u32)i;
+}
+
+__global__ void k_gather_sorted(const u32* order, const u64* key, const u64* cnt, const int* cid,
+                                u64 n, Grid res, long long* tx, long long* ty, u64* cnt_out,
+                                long long* cid_out) {
+    const u64 ymask = (1ull << res.bits_y) - 1;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 j = order[i];
+        const u64 k = key[j];
+        if (tx) tx[i] = res.origin_x + (long long)(k >> res.bits_y);
+        if (ty) ty[i] = res.origin_y + (long long)(k & ymask);
+        if (cnt_out) cnt_out[i] = cnt[j];
+        if (cid_out) cid_out[i] = cid ? (long long)cid[j] : -1ll;
+    }
+}
+
+__global__ void k_cluster_facts(const u64* root_key_sorted, const u32* root_idx_sorted, u64 n,
+                                const u32* size, const u64* npts, Grid res, u64* n_tiles,
+                                u64* n_points, long long* fx, long long* fy) {
+    const u64 ymask = (1ull << res.bits_y) - 1;
+    for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < n;
+         k += (u64)gridDim.x * blockDim.x) {
+        const u32 r = root_idx_sorted[k];
+        const u64 key = root_key_sorted[k];
+        if (n_tiles) n_tiles[k] = size[r];
+        if (n_points) n_points[k] = npts[r];
+        if (fx) fx[k] = res.origin_x + (long long)(key >> res.bits_y);
+        if (fy) fy[k] = res.origin_y + (long long)(key & ymask);
+    }
+}
+
+__global__ void k_count_of(Table t, u64 key, u64* out) {
+    const u64 v = table_find(t, key);
+    *out = (v == kEmpty) ? 0 : v;
+}
+
+int grid_for(u64 n, int n_sm, int per_sm = 8) {
+    const u64 want = (n + 255) / 256;
+    const u64 cap = (u64)n_sm * per_sm;
+    return (int)(want == 0 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+namespace rg {
+cudaError_t launch_iota(u32* out, u64 n, int n_sm, cudaStream_t st) {
+    k_iota<<<grid_for(n, n_sm), 256, 0, st>>>(out, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_gather_sorted(const u32* order, const u64* key, const u64* cnt,
+                                 const int* cid, u64 n, Grid res, long long* tx, long long* ty,
+                                 u64* cnt_out, long long* cid_out, int n_sm, cudaStream_t st) {
+    k_gather_sorted<<<grid_for(n, n_sm), 256, 0, st>>>(order, key, cnt, cid, n, res, tx, ty,
+                                                        cnt_out, cid_out);
+    return cudaGetLastError();
+}
+}  // namespace rg
+
+struct rg_ctx {
+    rg_params p{};
+    Grid grid{};  // canvas packing (ingest)
+    Grid res{};   // packing of the current significant set
+    bool res_is_canvas = true;
+    int device = 0;
+    int n_sm = 148;
+    int max_warps = 0;
+    cudaStream_t own = nullptr, st = nullptr, copy_st = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+
+    Slot* slots = nullptr;
+    u64 cap = 0;
+    Counters* ctr = nullptr;
+    Counters* hctr = nullptr;  // pinned mirror
+    Partial* part[2] = {nullptr, nullptr};
+    u64* scratch = nullptr;  // device scratch words
+
+    u64 used = 0, ingested = 0, skipped = 0, grows = 0;
+    enum State { kAccum, kSig, kAgg } state = kAccum;
+    bool table_dirty = false;  // holds pruned marks: clear before the next ingest
+
+    // significant set + agglomeration scratch, capacity sig_cap
+    u64 n_sig = 0, sig_cap = 0;
+    u64 *sig_key = nullptr, *sig_cnt = nullptr, *npts = nullptr, *min_key = nullptr;
+    u32 *parent = nullptr, *size = nullptr;
+    int *tile_cid = nullptr, *root_cid = nullptr;
+    u64 *root_key = nullptr, *root_key_sorted = nullptr;
+    u32 *root_idx = nullptr, *root_idx_sorted = nullptr;
+    void* sort_temp = nullptr;
+    size_t sort_temp_bytes = 0;
+    u64 n_roots = 0, n_kept = 0;
+
+    int2* offsets = nullptr;
+    int n_offsets = 0;
+
+    double* stage[2] = {nullptr, nullptr};
+    int* lstage[2] = {nullptr, nullptr};
+    u64 stage_pts = 0;
+
+    double ms_contract = 0, ms_prune = 0, ms_agg = 0, ms_label = 0;
+    u64 launches = 0;
+    std::string err;
+};
+
+namespace {
+
+rg_status set_err(rg_ctx* c, rg_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c)
+        c->err = buf;
+    else
+        g_create_error = buf;
+    return s;
+}
+
+rg_status cuda_err(rg_ctx* c, cudaError_t e, const char* what) {
+    return set_err(c, e == cudaErrorMemoryAllocation ? RG_ERR_OOM : RG_ERR_CUDA,
+                   "CUDA error in %s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call)                                                         \
+    do {                                                                 \
+        cudaError_t e_ = (call);                                         \
+        if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call);          \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, u64 count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc((void**)p, count * sizeof(T));
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+rg_status validate(const rg_params* p, std::string& msg) {
+    // GridParams::validate core.hpp:98-115, same checks, same order, same text.
+    const double s = std::pow(10.0, p->precision);
+    if (!std::isfinite(s) || s <= 0.0) {
+        msg = "precision yields a non-finite or zero scale factor";
+        return RG_ERR_CONFIG;
+    }
+    if (!std::isfinite(p->x_min) || !std::isfinite(p->x_max) || !std::isfinite(p->y_min) ||
+        !std::isfinite(p->y_max)) {
+        msg = "canvas bounds must be finite";
+        return RG_ERR_CONFIG;
+    }
+    if (p->x_min >= p->x_max || p->y_min >= p->y_max) {
+        msg = "canvas bounds must satisfy x_min < x_max and y_min < y_max";
+        return RG_ERR_CONFIG;
+    }
+    const double limit = 4.6e18;
+    if (std::abs(p->x_min) * s > limit || std::abs(p->x_max) * s > limit ||
+        std::abs(p->y_min) * s > limit || std::abs(p->y_max) * s > limit) {
+        msg = "precision too high for the canvas extent (tile index overflow)";
+        return RG_ERR_CONFIG;
+    }
+    if (p->threshold < 1) {
+        msg = "threshold must be >= 1";
+        return RG_ERR_CONFIG;
+    }
+    if (p->distance < 1) {
+        msg = "distance must be >= 1";
+        return RG_ERR_CONFIG;
+    }
+    if (p->min_cluster_size < 1) {
+        msg = "min cluster size must be >= 1";
+        return RG_ERR_CONFIG;
+    }
+    if (p->metric != RG_METRIC_CHEBYSHEV && p->metric != RG_METRIC_MANHATTAN) {
+        msg = "unknown metric";
+        return RG_ERR_CONFIG;
+    }
+    if (p->mode != RG_MODE_COUNT_ONLY && p->mode != RG_MODE_RETAIN_POINTS) {
+        msg = "unknown mode";
+        return RG_ERR_CONFIG;
+    }
+    if (p->oob_policy != RG_OOB_SKIP && p->oob_policy != RG_OOB_STRICT) {
+        msg = "unknown out-of-bounds policy";
+        return RG_ERR_CONFIG;
+    }
+    // GPU-path limits.
+    if (p->dedupe_points) {
+        msg = "dedupe_points is not supported on the GPU path";
+        return RG_ERR_UNSUPPORTED;
+    }
+    if (p->distance > 64) {
+        msg = "distance > 64 is not supported on the GPU path";
+        return RG_ERR_UNSUPPORTED;
+    }
+    const double cols = std::floor(p->x_max * s) - std::floor(p->x_min * s) + 1.0;
+    const double rows = std::floor(p->y_max * s) - std::floor(p->y_min * s) + 1.0;
+    if (bits_for(cols) + bits_for(rows) > 63) {
+        msg = "canvas has too many tiles for a 63-bit packed tile key on the GPU path";
+        return RG_ERR_UNSUPPORTED;
+    }
+    return RG_OK;
+}
+
+Grid make_grid(const rg_params& p) {
+    Grid g{};
+    g.scale = std::pow(10.0, p.precision);  // GridParams::scale core.hpp:95
+    g.x_min = p.x_min;
+    g.x_max = p.x_max;
+    g.y_min = p.y_min;
+    g.y_max = p.y_max;
+    g.origin_x = (long long)std::floor(p.x_min * g.scale);  // min_column core.hpp:117-119
+    g.origin_y = (long long)std::floor(p.y_min * g.scale);
+    const double cols = std::floor(p.x_max * g.scale) - std::floor(p.x_min * g.scale) + 1.0;
+    const double rows = std::floor(p.y_max * g.scale) - std::floor(p.y_min * g.scale) + 1.0;
+    g.bits_x = bits_for(cols);
+    g.bits_y = bits_for(rows);
+    return g;
+}
+
+Table table_of(const rg_ctx* c) {
+    Table t;
+    t.slots = c->slots;
+    t.mask = c->cap - 1;
+    t.shift = 64 - log2u(c->cap);
+    return t;
+}
+
+rg_status alloc_table(rg_ctx* ctx, u64 cap, Slot** out) {
+    CK(dalloc(out, cap));
+    cudaError_t e = launch_table_clear(*out, cap, ctx->n_sm, ctx->st);
+    ++ctx->launches;
+    if (e != cudaSuccess) {
+        dfree(*out);
+        return cuda_err(ctx, e, "table clear");
+    }
+    return RG_OK;
+}
+
+// TileCounts::grow accumulator.hpp:84-94: allocate a larger table and fold the
+// old one into it.
+rg_status grow_table(rg_ctx* ctx, u64 new_cap) {
+    Slot* ns = nullptr;
+    rg_status s = alloc_table(ctx, new_cap, &ns);
+    if (s != RG_OK) return s;
+    if (ctx->slots) {
+        Table nt;
+        nt.slots = ns;
+        nt.mask = new_cap - 1;
+        nt.shift = 64 - log2u(new_cap);
+        CK(launch_table_fold(ctx->slots, ctx->cap, nt, ctx->scratch, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx->slots);
+        ++ctx->grows;
+    }
+    ctx->slots = ns;
+    ctx->cap = new_cap;
+    return RG_OK;
+}
+
+void zero_field(rg_ctx* ctx, u64* f) { cudaMemsetAsync(f, 0, sizeof(u64), ctx->st); }
+
+rg_status pull_counters(rg_ctx* ctx) {
+    CK(cudaMemcpyAsync(ctx->hctr, ctx->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->used = ctx->hctr->used;
+    ctx->ingested = ctx->hctr->ingested;
+    ctx->skipped = ctx->hctr->skipped;
+    return RG_OK;
+}
+
+rg_status push_counters(rg_ctx* ctx) {
+    ctx->hctr->used = ctx->used;
+    ctx->hctr->ingested = ctx->ingested;
+    ctx->hctr->skipped = ctx->skipped;
+    CK(cudaMemcpyAsync(&ctx->ctr->used, &ctx->hctr->used, 3 * sizeof(u64),
+                       cudaMemcpyHostToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+// Returns the accumulator to "fresh" after a prune consumed it
+// (accumulator.hpp:171-173: counts_.clear()). ingested/skipped are kept, as in
+// the reference.
+rg_status reopen_accumulator(rg_ctx* ctx) {
+    if (ctx->state == rg_ctx::kAccum && !ctx->table_dirty) return RG_OK;
+    if (ctx->slots) {
+        CK(launch_table_clear(ctx->slots, ctx->cap, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+    }
+    ctx->used = 0;
+    ctx->table_dirty = false;
+    ctx->state = rg_ctx::kAccum;
+    ctx->n_sig = 0;
+    ctx->n_roots = ctx->n_kept = 0;
+    ctx->res = ctx->grid;
+    ctx->res_is_canvas = true;
+    return push_counters(ctx);
+}
+
+struct PhaseTimer {
+    rg_ctx* c;
+    double* acc;
+    PhaseTimer(rg_ctx* c_, double* a) : c(c_), acc(a) { cudaEventRecord(c->t0, c->st); }
+    void stop() {
+        if (!acc) return;
+        cudaEventRecord(c->t1, c->st);
+        cudaEventSynchronize(c->t1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->t0, c->t1);
+        *acc += ms;
+        acc = nullptr;
+    }
+    ~PhaseTimer() { stop(); }
+};
+
+// K1 driver over a device-resident span (TileAccumulator::ingest
+// accumulator.hpp:120-134). Handles budget stops, growth and resumption.
+rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
+    if (n == 0) return RG_OK;
+    const u64 rows = (n + 31) / 32;
+    const u64 w0 = (u64)ctx->max_warps;
+    u64 rps = rows / (8 * w0);
+    rps = std::max<u64>(4, std::min<u64>(64, rps));
+    const u64 n_seg = (rows + rps - 1) / rps;
+    const u64 W = std::min(w0, n_seg);
+    const u64 cap_min = next_pow2(107 * W + 1024);
+
+    if (!ctx->slots) {
+        u64 want;
+        if (ctx->p.capacity_hint) {
+            want = (u64)((double)ctx->p.capacity_hint / kMaxLoad) + 1;
+        } else {
+            const double tb = rg_params_tile_bound(&ctx->p);
+            double est = std::min((double)(n / 32), tb);
+            want = (u64)(est / kMaxLoad) + 1;
+        }
+        want = std::max<u64>(std::max<u64>(want, cap_min), 1024);
+        rg_status s = grow_table(ctx, next_pow2(want));
+        if (s != RG_OK) return s;
+    } else if (ctx->cap < cap_min) {
+        rg_status s = grow_table(ctx, cap_min);
+        if (s != RG_OK) return s;
+    }
+
+    zero_field(ctx, &ctx->ctr->ticket);
+    zero_field(ctx, &ctx->ctr->n_partial);
+    zero_field(ctx, &ctx->ctr->partial_ticket);
+    zero_field(ctx, &ctx->ctr->stopped);
+
+    PhaseTimer timer(ctx, &ctx->ms_contract);
+    u64 n_partial_in = 0;
+    int pin = 0;
+    for (int round = 0;; ++round) {
+        u64 soft = (u64)(kMaxLoad * (double)ctx->cap);
+        while (ctx->used + 64 * W >= soft) {
+            rg_status s = grow_table(ctx, ctx->cap * 2);
+            if (s != RG_OK) return s;
+            soft = (u64)(kMaxLoad * (double)ctx->cap);
+        }
+        ContractLaunch L;
+        L.xy = xy;
+        L.n = n;
+        L.rows_per_seg = rps;
+        L.warps = W;
+        L.g = ctx->grid;
+        L.t = table_of(ctx);
+        L.ctr = ctx->ctr;
+        L.partial_in = ctx->part[pin];
+        L.n_partial_in = n_partial_in;
+        L.partial_out = ctx->part[1 - pin];
+        L.budget = (soft - ctx->used) / W;
+        CK(launch_contract(L, ctx->st));
+        ++ctx->launches;
+        rg_status s = pull_counters(ctx);
+        if (s != RG_OK) return s;
+        if (ctx->hctr->stopped == 0) break;
+        // Some warps ran out of budget: resume their partial segments (and
+        // the untouched tickets) after growing if the table is filling up.
+        n_partial_in = ctx->hctr->n_partial;
+        pin = 1 - pin;
+        zero_field(ctx, &ctx->ctr->n_partial);
+        zero_field(ctx, &ctx->ctr->partial_ticket);
+        zero_field(ctx, &ctx->ctr->stopped);
+        if (ctx->used >= (u64)(0.85 * kMaxLoad * (double)ctx->cap)) {
+            s = grow_table(ctx, ctx->cap * 2);
+            if (s != RG_OK) return s;
+        }
+        if (round > 64) return set_err(ctx, RG_ERR_CUDA, "contraction failed to make progress");
+    }
+    return RG_OK;
+}
+
+rg_status ensure_stage(rg_ctx* ctx, u64 pts, bool labels) {
+    const u64 want = std::min<u64>(pts, kStagePoints);
+    if (ctx->stage_pts < want) {
+        for (int b = 0; b < 2; ++b) {
+            dfree(ctx->stage[b]);
+            dfree(ctx->lstage[b]);
+        }
+        ctx->stage_pts = 0;
+        for (int b = 0; b < 2; ++b) CK(dalloc(&ctx->stage[b], 2 * want));
+        ctx->stage_pts = want;
+    }
+    if (labels && !ctx->lstage[0]) {
+        for (int b = 0; b < 2; ++b) CK(dalloc(&ctx->lstage[b], ctx->stage_pts));
+    }
+    return RG_OK;
+}
+
+// Strict policy: index of the first out-of-bounds point, or n.
+rg_status first_oob(rg_ctx* ctx, const double* dxy, u64 n, u64* first) {
+    CK(cudaMemsetAsync(&ctx->ctr->first_oob, 0xff, sizeof(u64), ctx->st));
+    CK(launch_first_oob(dxy, n, ctx->grid, &ctx->ctr->first_oob, ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    u64 f = 0;
+    CK(cudaMemcpyAsync(&ctx->hctr->first_oob, &ctx->ctr->first_oob, sizeof(u64),
+                       cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    f = ctx->hctr->first_oob;
+    *first = f < n ? f : n;
+    return RG_OK;
+}
+
+rg_status oob_error(rg_ctx* ctx, double x, double y) {
+    // accumulator.hpp:123-125: "point (" + to_string(x) + ", " + to_string(y) + ") ..."
+    // std::to_string(double) formats with "%f".
+    return set_err(ctx, RG_ERR_OOB, "point (%f, %f) outside canvas bounds", x, y);
+}
+
+rg_status ingest_span(rg_ctx* ctx, const double* dxy, u64 n, bool* hit_oob, double* ox,
+                      double* oy) {
+    *hit_oob = false;
+    if (ctx->p.oob_policy == RG_OOB_STRICT) {
+        u64 f = n;
+        rg_status s = first_oob(ctx, dxy, n, &f);
+        if (s != RG_OK) return s;
+        if (f < n) {
+            double pt[2];
+            CK(cudaMemcpy(pt, dxy + 2 * f, sizeof pt, cudaMemcpyDeviceToHost));
+            *hit_oob = true;
+            *ox = pt[0];
+            *oy = pt[1];
+            return ingest_device(ctx, dxy, f);
+        }
+    }
+    return ingest_device(ctx, dxy, n);
+}
+
+rg_status ingest_any(rg_ctx* ctx, const double* xy, u64 n, rg_memkind kind) {
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    if (n == 0) return RG_OK;
+    bool oob = false;
+    double ox = 0, oy = 0;
+    if (kind == RG_MEM_DEVICE) {
+        s = ingest_span(ctx, xy, n, &oob, &ox, &oy);
+        if (s != RG_OK) return s;
+        return oob ? oob_error(ctx, ox, oy) : RG_OK;
+    }
+    // Host span: double-buffered H2D staging overlapped with K1.
+    s = ensure_stage(ctx, n, false);
+    if (s != RG_OK) return s;
+    const u64 ch = ctx->stage_pts;
+    const u64 chunks = (n + ch - 1) / ch;
+    auto enqueue_copy = [&](u64 i) -> rg_status {
+        const int b = (int)(i & 1);
+        const u64 off = i * ch;
+        const u64 len = std::min(ch, n - off);
+        CK(cudaStreamWaitEvent(ctx->copy_st, ctx->done[b], 0));
+        CK(cudaMemcpyAsync(ctx->stage[b], xy + 2 * off, len * 2 * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->copy_st));
+        CK(cudaEventRecord(ctx->copied[b], ctx->copy_st));
+        return RG_OK;
+    };
+    for (u64 i = 0; i < std::min<u64>(2, chunks); ++i) {
+        s = enqueue_copy(i);
+        if (s != RG_OK) return s;
+    }
+    for (u64 i = 0; i < chunks; ++i) {
+        const int b = (int)(i & 1);
+        const u64 off = i * ch;
+        const u64 len = std::min(ch, n - off);
+        CK(cudaStreamWaitEvent(ctx->st, ctx->copied[b], 0));
+        s = ingest_span(ctx, ctx->stage[b], len, &oob, &ox, &oy);
+        if (s != RG_OK) return s;
+        CK(cudaEventRecord(ctx->done[b], ctx->st));
+        if (oob) {
+            CK(cudaStreamSynchronize(ctx->copy_st));
+            return oob_error(ctx, ox, oy);
+        }
+        if (i + 2 < chunks) {
+            s = enqueue_copy(i + 2);
+            if (s != RG_OK) return s;
+        }
+    }
+    CK(cudaStreamSynchronize(ctx->copy_st));
+    return RG_OK;
+}
+
+rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
+    if (ctx->sig_cap >= n && ctx->sig_key) return RG_OK;
+    dfree(ctx->sig_key);
+    dfree(ctx->sig_cnt);
+    dfree(ctx->npts);
+    dfree(ctx->min_key);
+    dfree(ctx->parent);
+    dfree(ctx->size);
+    dfree(ctx->tile_cid);
+    dfree(ctx->root_cid);
+    dfree(ctx->root_key);
+    dfree(ctx->root_key_sorted);
+    dfree(ctx->root_idx);
+    dfree(ctx->root_idx_sorted);
+    ctx->sig_cap = 0;
+    const u64 c = std::max<u64>(n, 1024);
+    CK(dalloc(&ctx->sig_key, c));
+    CK(dalloc(&ctx->sig_cnt, c));
+    CK(dalloc(&ctx->npts, c));
+    CK(dalloc(&ctx->min_key, c));
+    CK(dalloc(&ctx->parent, c));
+    CK(dalloc(&ctx->size, c));
+    CK(dalloc(&ctx->tile_cid, c));
+    CK(dalloc(&ctx->root_cid, c));
+    CK(dalloc(&ctx->root_key, c));
+    CK(dalloc(&ctx->root_key_sorted, c));
+    CK(dalloc(&ctx->root_idx, c));
+    CK(dalloc(&ctx->root_idx_sorted, c));
+    ctx->sig_cap = c;
+    return RG_OK;
+}
+
+rg_status ensure_sort_temp(rg_ctx* ctx, u64 n, int bits) {
+    const size_t need = sort_pairs_temp_bytes(std::max<u64>(n, 1), bits);
+    if (ctx->sort_temp_bytes >= need && ctx->sort_temp) return RG_OK;
+    dfree(ctx->sort_temp);
+    ctx->sort_temp_bytes = 0;
+    CK(cudaMalloc(&ctx->sort_temp, need));
+    ctx->sort_temp_bytes = need;
+    return RG_OK;
+}
+
+rg_status prune_impl(rg_ctx* ctx) {
+    if (ctx->state != rg_ctx::kAccum) {
+        // prune() on a consumed accumulator returns nothing (empty table).
+        rg_status s = reopen_accumulator(ctx);
+        if (s != RG_OK) return s;
+    }
+    rg_status s = ensure_sig_capacity(ctx, ctx->used);
+    if (s != RG_OK) return s;
+    PhaseTimer timer(ctx, &ctx->ms_prune);
+    zero_field(ctx, &ctx->ctr->n_sig);
+    if (ctx->slots && ctx->used) {
+        CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
+                          ctx->parent, ctx->ctr, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+    }
+    CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, sizeof(u64), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    timer.stop();
+    ctx->n_sig = ctx->hctr->n_sig;
+    ctx->state = rg_ctx::kSig;
+    ctx->table_dirty = true;
+    ctx->res = ctx->grid;
+    ctx->res_is_canvas = true;
+    ctx->n_roots = ctx->n_kept = 0;
+    return RG_OK;
+}
+
+rg_status agglomerate_impl(rg_ctx* ctx) {
+    if (ctx->state == rg_ctx::kAccum)
+        return set_err(ctx, RG_ERR_STATE, "agglomerate requires a pruned or loaded tile set");
+    PhaseTimer timer(ctx, &ctx->ms_agg);
+    ctx->n_roots = ctx->n_kept = 0;
+    if (ctx->n_sig == 0) {
+        ctx->state = rg_ctx::kAgg;
+        return RG_OK;
+    }
+    AggLaunch A;
+    A.sig_key = ctx->sig_key;
+    A.sig_cnt = ctx->sig_cnt;
+    A.n_sig_dev = &ctx->ctr->n_sig;
+    A.n_sig = ctx->n_sig;
+    A.t = table_of(ctx);
+    A.bits_y = ctx->res.bits_y;
+    A.bits_x = ctx->res.bits_x;
+    A.offsets = ctx->offsets;
+    A.n_offsets = ctx->n_offsets;
+    A.mu = ctx->p.min_cluster_size;
+    A.parent = ctx->parent;
+    A.size = ctx->size;
+    A.npts = ctx->npts;
+    A.min_key = ctx->min_key;
+    A.root_cid = ctx->root_cid;
+    A.tile_cid = ctx->tile_cid;
+    A.root_key = ctx->root_key;
+    A.root_idx = ctx->root_idx;
+    A.root_key_sorted = ctx->root_key_sorted;
+    A.root_idx_sorted = ctx->root_idx_sorted;
+    A.ctr = ctx->ctr;
+    A.n_sm = ctx->n_sm;
+    zero_field(ctx, &ctx->ctr->n_roots);
+    zero_field(ctx, &ctx->ctr->n_kept);
+    CK(launch_agglomerate(A, ctx->st));
+    ctx->launches += 4;
+    CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
+                       cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->n_roots = ctx->hctr->n_roots;
+    ctx->n_kept = ctx->hctr->n_kept;
+    rg_status s = ensure_sort_temp(ctx, ctx->n_kept, (int)(ctx->res.bits_x + ctx->res.bits_y));
+    if (s != RG_OK) return s;
+    A.sort_temp = ctx->sort_temp;
+    A.sort_temp_bytes = ctx->sort_temp_bytes;
+    CK(launch_order_and_label(A, ctx->n_kept, ctx->st));
+    ctx->launches += ctx->n_kept ? 5 : 1;  // cub onesweep passes + ids + labels (approx.)
+    CK(cudaStreamSynchronize(ctx->st));
+    timer.stop();
+    ctx->state = rg_ctx::kAgg;
+    return RG_OK;
+}
+
+bool same_params(const rg_params& a, const rg_params& b) {
+    return a.precision == b.precision && a.x_min == b.x_min && a.x_max == b.x_max &&
+           a.y_min == b.y_min && a.y_max == b.y_max;
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+
+extern "C" {
+
+int rg_abi_version(void) { return RG_ABI_VERSION; }
+
+const char* rg_status_string(rg_status s) {
+    switch (s) {
+        case RG_OK: return "ok";
+        case RG_ERR_CONFIG: return "config error";
+        case RG_ERR_OOB: return "out of bounds";
+        case RG_ERR_CUDA: return "cuda error";
+        case RG_ERR_OOM: return "out of device memory";
+        case RG_ERR_STATE: return "invalid state";
+        case RG_ERR_ARG: return "invalid argument";
+        case RG_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown";
+}
+
+int rg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int usable = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10 &&
+            prop.minor == 0)
+            ++usable;
+    }
+    return usable;
+}
+
+void rg_params_default(rg_params* out) {
+    if (!out) return;
+    std::memset(out, 0, sizeof *out);
+    out->precision = 3.5;
+    out->x_min = -180.0;
+    out->x_max = 180.0;
+    out->y_min = -90.0;
+    out->y_max = 90.0;
+    out->threshold = 5;
+    out->distance = 1;
+    out->metric = RG_METRIC_CHEBYSHEV;
+    out->min_cluster_size = 4;
+    out->mode = RG_MODE_COUNT_ONLY;
+    out->oob_policy = RG_OOB_SKIP;
+}
+
+rg_status rg_params_validate(const rg_params* p, char* err, size_t err_len) {
+    if (!p) return RG_ERR_ARG;
+    std::string msg;
+    rg_status s = validate(p, msg);
+    if (err && err_len) {
+        std::snprintf(err, err_len, "%s", msg.c_str());
+    }
+    return s;
+}
+
+double rg_params_scale(const rg_params* p) { return std::pow(10.0, p->precision); }
+
+int64_t rg_params_min_column(const rg_params* p) {
+    return (int64_t)std::floor(p->x_min * rg_params_scale(p));
+}
+
+int64_t rg_params_max_column(const rg_params* p) {
+    return (int64_t)std::floor(p->x_max * rg_params_scale(p));
+}
+
+double rg_params_tile_bound(const rg_params* p) {
+    // GridParams::tile_bound core.hpp:126-131
+    const double s = rg_params_scale(p);
+    const double cols = std::floor(p->x_max * s) - std::floor(p->x_min * s) + 1.0;
+    const double rows = std::floor(p->y_max * s) - std::floor(p->y_min * s) + 1.0;
+    return cols * rows;
+}
+
+const char* rg_last_error(const rg_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
+    if (!p || !out) return set_err(nullptr, RG_ERR_ARG, "null argument");
+    *out = nullptr;
+    std::string msg;
+    rg_status vs = validate(p, msg);
+    if (vs != RG_OK) return set_err(nullptr, vs, "%s", msg.c_str());
+    int n_dev = 0;
+    cudaError_t e = cudaGetDeviceCount(&n_dev);
+    if (e != cudaSuccess || n_dev == 0) {
+        cudaGetLastError();
+        return set_err(nullptr, RG_ERR_CUDA, "no CUDA device available (%s)",
+                       e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    }
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= n_dev) return set_err(nullptr, RG_ERR_ARG, "device %d out of range", device);
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) return set_err(nullptr, RG_ERR_CUDA, "%s", cudaGetErrorString(e));
+    if (prop.major != 10 || prop.minor != 0)
+        return set_err(nullptr, RG_ERR_CUDA,
+                       "device %d is sm_%d%d; this library is built for sm_100a only", device,
+                       prop.major, prop.minor);
+    DevGuard guard(device);
+    rg_ctx* ctx = new rg_ctx();
+    ctx->p = *p;
+    ctx->device = device;
+    ctx->n_sm = prop.multiProcessorCount;
+    ctx->grid = make_grid(*p);
+    ctx->res = ctx->grid;
+    ctx->max_warps = contract_max_warps(ctx->n_sm);
+    auto fail = [&](cudaError_t err, const char* what) {
+        set_err(nullptr, err == cudaErrorMemoryAllocation ? RG_ERR_OOM : RG_ERR_CUDA,
+                "CUDA error in %s: %s", what, cudaGetErrorString(err));
+        rg_destroy(ctx);
+        return err == cudaErrorMemoryAllocation ? RG_ERR_OOM : RG_ERR_CUDA;
+    };
+    if ((e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "stream");
+    ctx->st = ctx->own;
+    if ((e = cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "stream");
+    if ((e = cudaEventCreate(&ctx->t0)) != cudaSuccess) return fail(e, "event");
+    if ((e = cudaEventCreate(&ctx->t1)) != cudaSuccess) return fail(e, "event");
+    for (int b = 0; b < 2; ++b) {
+        if ((e = cudaEventCreateWithFlags(&ctx->copied[b], cudaEventDisableTiming)) !=
+            cudaSuccess)
+            return fail(e, "event");
+        if ((e = cudaEventCreateWithFlags(&ctx->done[b], cudaEventDisableTiming)) != cudaSuccess)
+            return fail(e, "event");
+    }
+    if ((e = dalloc(&ctx->ctr, 1)) != cudaSuccess) return fail(e, "cudaMalloc counters");
+    if ((e = cudaMallocHost((void**)&ctx->hctr, sizeof(Counters))) != cudaSuccess)
+        return fail(e, "cudaMallocHost");
+    std::memset(ctx->hctr, 0, sizeof(Counters));
+    if ((e = cudaMemset(ctx->ctr, 0, sizeof(Counters))) != cudaSuccess)
+        return fail(e, "cudaMemset");
+    for (int b = 0; b < 2; ++b)
+        if ((e = dalloc(&ctx->part[b], (u64)ctx->max_warps)) != cudaSuccess)
+            return fail(e, "cudaMalloc partials");
+    if ((e = dalloc(&ctx->scratch, 8)) != cudaSuccess) return fail(e, "cudaMalloc scratch");
+    const std::vector<int2> off = forward_offsets(*p);
+    ctx->n_offsets = (int)off.size();
+    if ((e = dalloc(&ctx->offsets, off.size())) != cudaSuccess) return fail(e, "cudaMalloc");
+    if ((e = cudaMemcpy(ctx->offsets, off.data(), off.size() * sizeof(int2),
+                        cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e, "cudaMemcpy offsets");
+    *out = ctx;
+    return RG_OK;
+}
+
+void rg_destroy(rg_ctx* ctx) {
+    if (!ctx) return;
+    DevGuard guard(ctx->device);
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    if (ctx->copy_st) cudaStreamSynchronize(ctx->copy_st);
+    dfree(ctx->slots);
+    dfree(ctx->ctr);
+    if (ctx->hctr) cudaFreeHost(ctx->hctr);
+    dfree(ctx->part[0]);
+    dfree(ctx->part[1]);
+    dfree(ctx->scratch);
+    dfree(ctx->sig_key);
+    dfree(ctx->sig_cnt);
+    dfree(ctx->npts);
+    dfree(ctx->min_key);
+    dfree(ctx->parent);
+    dfree(ctx->size);
+    dfree(ctx->tile_cid);
+    dfree(ctx->root_cid);
+    dfree(ctx->root_key);
+    dfree(ctx->root_key_sorted);
+    dfree(ctx->root_idx);
+    dfree(ctx->root_idx_sorted);
+    dfree(ctx->sort_temp);
+    dfree(ctx->offsets);
+    for (int b = 0; b < 2; ++b) {
+        dfree(ctx->stage[b]);
+        dfree(ctx->lstage[b]);
+        if (ctx->copied[b]) cudaEventDestroy(ctx->copied[b]);
+        if (ctx->done[b]) cudaEventDestroy(ctx->done[b]);
+    }
+    if (ctx->t0) cudaEventDestroy(ctx->t0);
+    if (ctx->t1) cudaEventDestroy(ctx->t1);
+    if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+rg_status rg_set_stream(rg_ctx* ctx, void* stream) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->st = stream ? (cudaStream_t)stream : ctx->own;
+    return RG_OK;
+}
+
+rg_status rg_synchronize(rg_ctx* ctx) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
+    DevGuard guard(ctx->device);
+    return ingest_any(ctx, xy, n, kind);
+}
+
+rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
+    rg_ctx* ctx = dst;
+    if (!dst || !src) return RG_ERR_ARG;
+    if (dst == src) return set_err(dst, RG_ERR_ARG, "cannot merge an accumulator into itself");
+    if (!same_params(dst->p, src->p))
+        return set_err(dst, RG_ERR_CONFIG, "merge requires equal grid parameters");
+    if (dst->device != src->device)
+        return set_err(dst, RG_ERR_UNSUPPORTED, "merge across devices is not supported");
+    DevGuard guard(dst->device);
+    rg_status s = reopen_accumulator(dst);
+    if (s != RG_OK) return s;
+    {
+        rg_ctx* c2 = src;
+        if (c2->state != rg_ctx::kAccum) {
+            s = reopen_accumulator(c2);
+            if (s != RG_OK) return set_err(dst, s, "%s", c2->err.c_str());
+        }
+        cudaStreamSynchronize(c2->st);
+    }
+    if (src->slots && src->used) {
+        const u64 need = (u64)((double)(dst->used + src->used) / kMaxLoad) + 1;
+        if (!dst->slots || dst->cap < need) {
+            s = grow_table(dst, next_pow2(std::max<u64>(need, 1024)));
+            if (s != RG_OK) return s;
+        }
+        CK(cudaMemsetAsync(dst->scratch, 0, sizeof(u64), dst->st));
+        CK(launch_table_fold(src->slots, src->cap, table_of(dst), dst->scratch, dst->n_sm,
+                             dst->st));
+        ++dst->launches;
+        u64 claimed = 0;
+        CK(cudaMemcpyAsync(&dst->hctr->pad0[0], dst->scratch, sizeof(u64),
+                           cudaMemcpyDeviceToHost, dst->st));
+        CK(cudaStreamSynchronize(dst->st));
+        claimed = dst->hctr->pad0[0];
+        dst->used += claimed;
+    }
+    dst->ingested += src->ingested;
+    dst->skipped += src->skipped;
+    s = push_counters(dst);
+    if (s != RG_OK) return s;
+    // Leave src empty (accumulator.hpp:150-153).
+    {
+        DevGuard g2(src->device);
+        rg_ctx* c2 = src;
+        if (c2->slots) {
+            cudaError_t e = launch_table_clear(c2->slots, c2->cap, c2->n_sm, c2->st);
+            ++c2->launches;
+            if (e != cudaSuccess) return cuda_err(dst, e, "clear merged source");
+        }
+        c2->used = c2->ingested = c2->skipped = 0;
+        s = push_counters(c2);
+        if (s != RG_OK) return set_err(dst, s, "%s", c2->err.c_str());
+    }
+    return RG_OK;
+}
+
+rg_status rg_entry_count(rg_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    *out = ctx->state == rg_ctx::kAccum ? ctx->used : 0;
+    return RG_OK;
+}
+
+rg_status rg_total_ingested(rg_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    *out = ctx->ingested;
+    return RG_OK;
+}
+
+rg_status rg_skipped(rg_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    *out = ctx->skipped;
+    return RG_OK;
+}
+
+rg_status rg_count_of(rg_ctx* ctx, int64_t tx, int64_t ty, uint64_t* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    *out = 0;
+    if (ctx->state != rg_ctx::kAccum || !ctx->slots || ctx->used == 0) return RG_OK;
+    const Grid& g = ctx->grid;
+    const long long kx = tx - g.origin_x, ky = ty - g.origin_y;
+    if (kx < 0 || ky < 0 || kx >= (1ll << g.bits_x) || ky >= (1ll << g.bits_y)) return RG_OK;
+    DevGuard guard(ctx->device);
+    const u64 key = ((u64)kx << g.bits_y) | (u64)ky;
+    k_count_of<<<1, 1, 0, ctx->st>>>(table_of(ctx), key, ctx->scratch);
+    ++ctx->launches;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&ctx->hctr->pad0[1], ctx->scratch, sizeof(u64), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    *out = ctx->hctr->pad0[1];
+    return RG_OK;
+}
+
+rg_status rg_export_counts(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* count, uint64_t cap,
+                           uint64_t* n_out) {
+    if (!ctx) return RG_ERR_ARG;
+    if (ctx->state != rg_ctx::kAccum || !ctx->slots || ctx->used == 0) {
+        if (n_out) *n_out = 0;
+        return RG_OK;
+    }
+    DevGuard guard(ctx->device);
+    std::vector<Slot> host(ctx->cap);
+    CK(cudaMemcpyAsync(host.data(), ctx->slots, ctx->cap * sizeof(Slot), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    std::vector<std::pair<u64, u64>> rows;
+    rows.reserve(ctx->used);
+    for (const Slot& s : host)
+        if (s.key != kEmpty) rows.emplace_back(s.key, s.count);
+    std::sort(rows.begin(), rows.end());
+    const Grid& g = ctx->grid;
+    const u64 ymask = (1ull << g.bits_y) - 1;
+    const u64 w = std::min<u64>(cap, rows.size());
+    for (u64 i = 0; i < w; ++i) {
+        if (tx) tx[i] = g.origin_x + (long long)(rows[i].first >> g.bits_y);
+        if (ty) ty[i] = g.origin_y + (long long)(rows[i].first & ymask);
+        if (count) count[i] = rows[i].second;
+    }
+    if (n_out) *n_out = rows.size();
+    return RG_OK;
+}
+
+rg_status rg_prune(rg_ctx* ctx, uint64_t* n_significant) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    rg_status s = prune_impl(ctx);
+    if (s == RG_OK && n_significant) *n_significant = ctx->n_sig;
+    return s;
+}
+
+rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
+                              const uint64_t* count, uint64_t n, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && (!tx || !ty)) return set_err(ctx, RG_ERR_ARG, "null tile buffer");
+    if (n >= 0x7fffffffull) return set_err(ctx, RG_ERR_UNSUPPORTED, "too many tiles");
+    DevGuard guard(ctx->device);
+    // Tile extents decide the key packing: the canvas packing when every tile
+    // lies on the canvas (then labelling points works), else a packing that
+    // covers the tiles' bounding box.
+    std::vector<int64_t> hx, hy;
+    const int64_t* px = tx;
+    const int64_t* py = ty;
+    if (kind == RG_MEM_DEVICE && n) {
+        hx.resize(n);
+        hy.resize(n);
+        CK(cudaMemcpy(hx.data(), tx, n * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hy.data(), ty, n * 8, cudaMemcpyDeviceToHost));
+        px = hx.data();
+        py = hy.data();
+    }
+    long long mnx = 0, mxx = 0, mny = 0, mxy = 0;
+    for (u64 i = 0; i < n; ++i) {
+        if (i == 0 || px[i] < mnx) mnx = px[i];
+        if (i == 0 || px[i] > mxx) mxx = px[i];
+        if (i == 0 || py[i] < mny) mny = py[i];
+        if (i == 0 || py[i] > mxy) mxy = py[i];
+    }
+    const Grid& g = ctx->grid;
+    Grid res = g;
+    bool on_canvas = n == 0 || (mnx >= g.origin_x && mny >= g.origin_y &&
+                                (u64)(mxx - g.origin_x) < (1ull << g.bits_x) &&
+                                (u64)(mxy - g.origin_y) < (1ull << g.bits_y));
+    if (!on_canvas) {
+        const double w = (double)mxx - (double)mnx + 1.0;
+        const double h = (double)mxy - (double)mny + 1.0;
+        const u32 bx = bits_for(w), by = bits_for(h);
+        if (bx + by > 63)
+            return set_err(ctx, RG_ERR_UNSUPPORTED,
+                           "tile set spans too large a range for a 63-bit packed key");
+        res.origin_x = mnx;
+        res.origin_y = mny;
+        res.bits_x = bx;
+        res.bits_y = by;
+    }
+    // Fresh table sized for n keys.
+    ctx->state = rg_ctx::kAccum;
+    ctx->table_dirty = true;
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    const u64 need = next_pow2(std::max<u64>((u64)((double)n / 0.5) + 1, 1024));
+    if (!ctx->slots || ctx->cap < need) {
+        if (ctx->slots) dfree(ctx->slots);
+        ctx->cap = 0;
+        s = alloc_table(ctx, need, &ctx->slots);
+        if (s != RG_OK) return s;
+        ctx->cap = need;
+    }
+    s = ensure_sig_capacity(ctx, n);
+    if (s != RG_OK) return s;
+    if (n) {
+        long long *dtx = nullptr, *dty = nullptr;
+        u64* dcnt = nullptr;
+        CK(dalloc(&dtx, n));
+        CK(dalloc(&dty, n));
+        if (count) CK(dalloc(&dcnt, n));
+        const cudaMemcpyKind mk =
+            kind == RG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(dtx, tx, n * 8, mk, ctx->st));
+        CK(cudaMemcpyAsync(dty, ty, n * 8, mk, ctx->st));
+        if (count) CK(cudaMemcpyAsync(dcnt, count, n * 8, mk, ctx->st));
+        CK(launch_load_tiles(dtx, dty, dcnt, n, res.origin_x, res.origin_y, res.bits_y,
+                             table_of(ctx), ctx->sig_key, ctx->sig_cnt, ctx->parent, ctx->n_sm,
+                             ctx->st));
+        ++ctx->launches;
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(dtx);
+        dfree(dty);
+        dfree(dcnt);
+    }
+    ctx->hctr->n_sig = n;
+    CK(cudaMemcpyAsync(&ctx->ctr->n_sig, &ctx->hctr->n_sig, sizeof(u64), cudaMemcpyHostToDevice,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->used = n;
+    ctx->n_sig = n;
+    ctx->res = res;
+    ctx->res_is_canvas = on_canvas;
+    ctx->state = rg_ctx::kSig;
+    ctx->table_dirty = true;
+    return RG_OK;
+}
+
+rg_status rg_agglomerate(rg_ctx* ctx, uint64_t* n_clusters) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    rg_status s = agglomerate_impl(ctx);
+    if (s == RG_OK && n_clusters) *n_clusters = ctx->n_kept;
+    return s;
+}
+
+rg_status rg_get_stats(rg_ctx* ctx, rg_stats* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    std::memset(out, 0, sizeof *out);
+    out->n_points = ctx->ingested + ctx->skipped;
+    out->n_ingested = ctx->ingested;
+    out->n_skipped = ctx->skipped;
+    out->peak_accumulator_entries = ctx->used;
+    out->n_significant = ctx->state == rg_ctx::kAccum ? 0 : ctx->n_sig;
+    out->n_components = ctx->n_roots;
+    out->n_clusters = ctx->n_kept;
+    out->table_capacity = ctx->cap;
+    out->table_grows = ctx->grows;
+    out->ms_contract = ctx->ms_contract;
+    out->ms_prune = ctx->ms_prune;
+    out->ms_agglomerate = ctx->ms_agg;
+    out->ms_label = ctx->ms_label;
+    return RG_OK;
+}
+
+rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
+                     rg_stats* stats) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
+    DevGuard guard(ctx->device);
+    // cluster_sequential builds a fresh accumulator (pipeline.hpp:98).
+    ctx->state = rg_ctx::kAccum;
+    ctx->table_dirty = true;
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    ctx->ingested = ctx->skipped = 0;
+    s = push_counters(ctx);
+    if (s != RG_OK) return s;
+    ctx->ms_contract = ctx->ms_prune = ctx->ms_agg = ctx->ms_label = 0;
+    s = ingest_any(ctx, xy, n, kind);
+    if (s != RG_OK) return s;
+    const u64 peak = ctx->used;
+    s = prune_impl(ctx);
+    if (s != RG_OK) return s;
+    s = agglomerate_impl(ctx);
+    if (s != RG_OK) return s;
+    ctx->used = peak;  // peak_accumulator_entries pipeline.hpp:100
+    if (stats) return rg_get_stats(ctx, stats);
+    return RG_OK;
+}
+
+rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* count,
+                             int64_t* cluster_id, uint64_t cap, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (ctx->state == rg_ctx::kAccum)
+        return set_err(ctx, RG_ERR_STATE, "no significant tiles: call rg_prune first");
+    DevGuard guard(ctx->device);
+    const u64 n = ctx->n_sig;
+    const u64 w = std::min<u64>(cap, n);
+    if (w == 0) return RG_OK;
+    const int bits = (int)(ctx->res.bits_x + ctx->res.bits_y);
+    u64* ks = nullptr;
+    u32 *iota = nullptr, *order = nullptr;
+    CK(dalloc(&ks, n));
+    CK(dalloc(&iota, n));
+    CK(dalloc(&order, n));
+    void* temp = nullptr;
+    const size_t tb = sort_pairs_temp_bytes(n, bits);
+    CK(cudaMalloc(&temp, tb));
+    CK(launch_iota(iota, n, ctx->n_sm, ctx->st));
+    CK(sort_pairs(temp, tb, ctx->sig_key, ks, iota, order, n, bits, ctx->st));
+    ctx->launches += 6;
+    long long *dtx = (long long*)tx, *dty = (long long*)ty, *dcid = (long long*)cluster_id;
+    u64* dcnt = (u64*)count;
+    if (kind == RG_MEM_HOST) {
+        dtx = dty = dcid = nullptr;
+        dcnt = nullptr;
+        if (tx) CK(dalloc(&dtx, w));
+        if (ty) CK(dalloc(&dty, w));
+        if (count) CK(dalloc(&dcnt, w));
+        if (cluster_id) CK(dalloc(&dcid, w));
+    }
+    CK(launch_gather_sorted(order, ctx->sig_key, ctx->sig_cnt,
+                            ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr, w, ctx->res,
+                            dtx, dty, dcnt, dcid, ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    if (kind == RG_MEM_HOST) {
+        if (tx) CK(cudaMemcpyAsync(tx, dtx, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (ty) CK(cudaMemcpyAsync(ty, dty, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (count) CK(cudaMemcpyAsync(count, dcnt, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (cluster_id) CK(cudaMemcpyAsync(cluster_id, dcid, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    if (kind == RG_MEM_HOST) {
+        dfree(dtx);
+        dfree(dty);
+        dfree(dcnt);
+        dfree(dcid);
+    }
+    cudaFree(temp);
+    dfree(ks);
+    dfree(iota);
+    dfree(order);
+    return RG_OK;
+}
+
+rg_status rg_get_clusters(rg_ctx* ctx, uint64_t* n_tiles, uint64_t* n_points, int64_t* first_tx,
+                          int64_t* first_ty, uint64_t cap, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (ctx->state != rg_ctx::kAgg)
+        return set_err(ctx, RG_ERR_STATE, "no clusters: call rg_agglomerate first");
+    DevGuard guard(ctx->device);
+    const u64 w = std::min<u64>(cap, ctx->n_kept);
+    if (w == 0) return RG_OK;
+    u64 *dnt = (u64*)n_tiles, *dnp = (u64*)n_points;
+    long long *dfx = (long long*)first_tx, *dfy = (long long*)first_ty;
+    if (kind == RG_MEM_HOST) {
+        dnt = dnp = nullptr;
+        dfx = dfy = nullptr;
+        if (n_tiles) CK(dalloc(&dnt, w));
+        if (n_points) CK(dalloc(&dnp, w));
+        if (first_tx) CK(dalloc(&dfx, w));
+        if (first_ty) CK(dalloc(&dfy, w));
+    }
+    k_cluster_facts<<<grid_for(w, ctx->n_sm), 256, 0, ctx->st>>>(
+        ctx->root_key_sorted, ctx->root_idx_sorted, w, ctx->size, ctx->npts, ctx->res, dnt, dnp,
+        dfx, dfy);
+    ++ctx->launches;
+    CK(cudaGetLastError());
+    if (kind == RG_MEM_HOST) {
+        if (n_tiles) CK(cudaMemcpyAsync(n_tiles, dnt, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (n_points) CK(cudaMemcpyAsync(n_points, dnp, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (first_tx) CK(cudaMemcpyAsync(first_tx, dfx, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+        if (first_ty) CK(cudaMemcpyAsync(first_ty, dfy, w * 8, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    if (kind == RG_MEM_HOST) {
+        dfree(dnt);
+        dfree(dnp);
+        dfree(dfx);
+        dfree(dfy);
+    }
+    return RG_OK;
+}
+
+rg_status rg_device_result(rg_ctx* ctx, rg_device_view* out) {
+    if (!ctx || !out) return RG_ERR_ARG;
+    if (ctx->state == rg_ctx::kAccum)
+        return set_err(ctx, RG_ERR_STATE, "no significant tiles: call rg_prune first");
+    out->key = (const uint64_t*)ctx->sig_key;
+    out->count = (const uint64_t*)ctx->sig_cnt;
+    out->cluster_id = ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr;
+    out->n_significant = ctx->n_sig;
+    out->n_clusters = ctx->n_kept;
+    out->origin_x = ctx->res.origin_x;
+    out->origin_y = ctx->res.origin_y;
+    out->key_bits_y = ctx->res.bits_y;
+    out->reserved = 0;
+    return RG_OK;
+}
+
+void rg_decode_key(const rg_device_view* v, uint64_t key, int64_t* tx, int64_t* ty) {
+    if (tx) *tx = v->origin_x + (int64_t)(key >> v->key_bits_y);
+    if (ty) *ty = v->origin_y + (int64_t)(key & ((1ull << v->key_bits_y) - 1));
+}
+
+rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* labels,
+                          rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && (!xy || !labels)) return set_err(ctx, RG_ERR_ARG, "null buffer");
+    if (ctx->state != rg_ctx::kAgg)
+        return set_err(ctx, RG_ERR_STATE, "labelling requires rg_agglomerate first");
+    if (!ctx->res_is_canvas)
+        return set_err(ctx, RG_ERR_UNSUPPORTED,
+                       "labelling points needs significant tiles on the canvas");
+    if (n == 0) return RG_OK;
+    DevGuard guard(ctx->device);
+    PhaseTimer timer(ctx, &ctx->ms_label);
+    if (!ctx->slots) {
+        // no table (empty significant set): every label is -1
+        if (kind == RG_MEM_DEVICE) {
+            CK(cudaMemsetAsync(labels, 0xff, n * sizeof(int32_t), ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+        } else {
+            std::memset(labels, 0xff, n * sizeof(int32_t));
+        }
+        return RG_OK;
+    }
+    if (kind == RG_MEM_DEVICE) {
+        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, labels, ctx->n_sm,
+                               ctx->st));
+        ++ctx->launches;
+        CK(cudaStreamSynchronize(ctx->st));
+        return RG_OK;
+    }
+    rg_status s = ensure_stage(ctx, n, true);
+    if (s != RG_OK) return s;
+    const u64 ch = ctx->stage_pts;
+    for (u64 off = 0; off < n; off += ch) {
+        const int b = (int)((off / ch) & 1);
+        const u64 len = std::min(ch, n - off);
+        CK(cudaMemcpyAsync(ctx->stage[b], xy + 2 * off, len * 16, cudaMemcpyHostToDevice,
+                           ctx->st));
+        CK(launch_label_points(ctx->stage[b], len, ctx->grid, table_of(ctx), ctx->tile_cid,
+                               ctx->lstage[b], ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(labels + off, ctx->lstage[b], len * 4, cudaMemcpyDeviceToHost,
+                           ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+uint64_t rg_kernel_launches(const rg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// common.cuh — device-side data layout shared by all RASTER kernels.
+//
+// Tile keys. The reference identifies a tile by raster::Tile{int64 x, int64 y}
+// with lexicographic order (core.hpp:48-54). On the device a tile is one
+// 64-bit packed key
+//      key = (tx - origin_x) << bits_y | (ty - origin_y)
+// with both fields non-negative and bits_x + bits_y <= 63, so unsigned key
+// order == lexicographic Tile order and the all-ones word can never be a key
+// (it is the EMPTY sentinel). For ingested points origin = (min_column,
+// min_row) of the canvas (core.hpp:117-122); monotonicity of IEEE
+// round-to-nearest multiplication guarantees every in-bounds point lands in
+// [origin, origin + 2^bits).
+//
+// Hash table. One open-addressed, linear-probing table of 16-byte slots
+// {u64 key, u64 count} in HBM replaces TileCounts (accumulator.hpp:23-99).
+// Keys are claimed with a 64-bit CAS and never change afterwards, so probes
+// may use plain (L1-cacheable) loads; counts are bumped with RED.ADD.64.
+// After pruning, the count word of a significant slot is overwritten with
+// SIG_BIT | dense_index so neighbour lookups and per-point labelling resolve
+// a key to its significant-tile index with one probe.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rg {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr u64 kEmpty = ~0ull;
+constexpr u64 kSigBit = 1ull << 63;
+constexpr u32 kFull = 0xffffffffu;
+
+struct __align__(16) Slot {
+    u64 key;
+    u64 count;
+};
+
+// Projection + packing parameters (host computes scale = pow(10, p) with the
+// same libm as the reference, core.hpp:95; the device never calls pow).
+struct Grid {
+    double scale;
+    double x_min, x_max, y_min, y_max;
+    long long origin_x, origin_y;
+    u32 bits_y;
+    u32 bits_x;
+};
+
+struct Table {
+    Slot* slots;
+    u64 mask;      // capacity - 1 (capacity is a power of two)
+    u32 shift;     // 64 - log2(capacity)
+};
+
+// Multiplicative (Fibonacci) hashing on the packed key; the reference's
+// TileHash (core.hpp:56-68) only affects probe order, never results.
+__device__ __forceinline__ u64 slot_of(u64 key, u32 shift) {
+    return (key * 0x9E3779B97F4A7C15ull) >> shift;
+}
+
+// Bounds::contains core.hpp:33-35 — closed interval; NaN compares false.
+__device__ __forceinline__ bool in_bounds(const Grid& g, double x, double y) {
+    return x >= g.x_min && x <= g.x_max && y >= g.y_min && y <= g.y_max;
+}
+
+// project_unchecked core.hpp:136-139: (int64)floor(x * s). __dmul_rn is the
+// IEEE double product (no FMA contraction can apply to a lone multiply, but
+// the intrinsic makes it explicit); cvt.rmi.s64.f64 floors and converts in
+// one instruction, identical to floor-then-cast for in-range values.
+__device__ __forceinline__ u64 pack_key(const Grid& g, double x, double y) {
+    const long long tx = __double2ll_rd(__dmul_rn(x, g.scale));
+    const long long ty = __double2ll_rd(__dmul_rn(y, g.scale));
+    return ((u64)(tx - g.origin_x) << g.bits_y) | (u64)(ty - g.origin_y);
+}
+
+__device__ __forceinline__ u64 ld_key(const Slot* s) {
+    u64 v;
+    asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(&s->key));
+    return v;
+}
+
+__device__ __forceinline__ void ld_slot(const Slot* s, u64& key, u64& val) {
+    asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(key), "=l"(val) : "l"(s));
+}
+
+__device__ __forceinline__ void red_add(u64* p, u64 v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Streaming 128-bit load of one point (read once: keep it out of L1 and
+// mark it evict-first in L2 so the hash table stays resident).
+__device__ __forceinline__ u64 evict_first_policy() {
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ double2 ld_point_stream(const double2* p, u64 pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+// Insert-or-add into the HBM table. Returns true when this call claimed a new
+// slot (a new distinct tile). TileCounts::add accumulator.hpp:33-50.
+__device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
+    u64 i = slot_of(key, t.shift);
+    while (true) {
+        Slot* s = t.slots + i;
+        u64 k = ld_key(s);
+        if (k == key) {
+            red_add(&s->count, cnt);
+            return false;
+        }
+        if (k == kEmpty) {
+            const u64 old = atomicCAS(&s->key, kEmpty, key);
+            if (old == kEmpty) {
+                red_add(&s->count, cnt);
+                return true;
+            }
+            if (old == key) {
+                red_add(&s->count, cnt);
+                return false;
+            }
+        }
+        i = (i + 1) & t.mask;
+    }
+}
+
+// Lookup: returns the slot's value word, or kEmpty when the key is absent.
+// TileCounts::count_of accumulator.hpp:53-61.
+__device__ __forceinline__ u64 table_find(const Table& t, u64 key) {
+    u64 i = slot_of(key, t.shift);
+    while (true) {
+        u64 k, v;
+        ld_slot(t.slots + i, k, v);
+        if (k == key) return v;
+        if (k == kEmpty) return kEmpty;
+        i = (i + 1) & t.mask;
+    }
+}
+
+// Device-side counters of one context (one cache line each to avoid false
+// sharing between the hot ones).
+struct Counters {
+    u64 ticket;          // next work segment (K1 / K4 dynamic scheduling)
+    u64 pad0[15];
+    u64 used;            // distinct keys in the table
+    u64 ingested;        // in-bounds points
+    u64 skipped;         // out-of-bounds points
+    u64 stopped;         // warps that exhausted their new-key budget
+    u64 n_partial;       // partially processed segments recorded
+    u64 partial_ticket;  // next partial segment to resume
+    u64 pad1[10];
+    u64 n_sig;           // significant tiles (K2)
+    u64 n_roots;         // components
+    u64 n_kept;          // clusters after the mu filter
+    u64 first_oob;       // strict policy: smallest out-of-bounds index
+    u64 pad2[12];
+};
+
+struct Partial {
+    u64 segment;
+    u64 next_row;
+};
+
+}  // namespace rg

@@ -1,0 +1,78 @@
+// internal.h — launch interfaces between the C-ABI layer (api.cu) and the
+// kernel translation units. Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rg {
+
+struct ContractLaunch {
+    const double* xy;
+    u64 n;
+    u64 rows_per_seg;
+    u64 warps;
+    Grid g;
+    Table t;
+    Counters* ctr;
+    const Partial* partial_in;
+    u64 n_partial_in;
+    Partial* partial_out;
+    u64 budget;
+};
+
+int contract_max_warps(int n_sm);
+cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st);
+cudaError_t launch_table_clear(Slot* slots, u64 n, int n_sm, cudaStream_t st);
+cudaError_t launch_table_fold(const Slot* src, u64 n_src, Table dst, u64* claimed, int n_sm,
+                              cudaStream_t st);
+cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
+                             cudaStream_t st);
+cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
+                           Counters* ctr, int n_sm, cudaStream_t st);
+
+struct AggLaunch {
+    const u64* sig_key;
+    const u64* sig_cnt;
+    const u64* n_sig_dev;  // device copy of S (&ctr->n_sig)
+    u64 n_sig;             // host copy of S (for sizing)
+    Table t;
+    u32 bits_y, bits_x;
+    const int2* offsets;
+    int n_offsets;
+    u64 mu;
+    u32* parent;
+    u32* size;
+    u64* npts;
+    u64* min_key;
+    int* root_cid;
+    int* tile_cid;
+    u64* root_key;
+    u32* root_idx;
+    u64* root_key_sorted;
+    u32* root_idx_sorted;
+    void* sort_temp;
+    size_t sort_temp_bytes;
+    Counters* ctr;
+    int n_sm;
+};
+
+cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st);
+cudaError_t launch_order_and_label(const AggLaunch& A, u64 n_kept, cudaStream_t st);
+size_t sort_pairs_temp_bytes(u64 n, int bits);
+cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_out,
+                       const u32* v_in, u32* v_out, u64 n, int bits, cudaStream_t st);
+cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
+                              long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                              u64* sig_cnt, u32* parent, int n_sm, cudaStream_t st);
+
+cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
+                                int* labels, int n_sm, cudaStream_t st);
+
+// small utility kernels (api.cu)
+cudaError_t launch_iota(u32* out, u64 n, int n_sm, cudaStream_t st);
+cudaError_t launch_gather_sorted(const u32* order, const u64* key, const u64* cnt,
+                                 const int* cid, u64 n, Grid res, long long* tx, long long* ty,
+                                 u64* cnt_out, long long* cid_out, int n_sm, cudaStream_t st);
+
+}  // namespace rg
