@@ -77,10 +77,19 @@ def build_oracle(verbose: bool = False) -> None:
         print(out.stdout)
 
 
+def build_cpp_tests(verbose: bool = False) -> None:
+    """C++ drop-in parity test (needs the reference headers; skipped if absent)."""
+    out = subprocess.run(["bash", str(ROOT / "tests" / "cpp" / "build.sh")], check=True,
+                         capture_output=not verbose, text=True)
+    if verbose and out.stdout:
+        print(out.stdout)
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_gpu(force, verbose)
     build_datagen(force, verbose)
     build_oracle(verbose)
+    build_cpp_tests(verbose)
 
 
 if __name__ == "__main__":

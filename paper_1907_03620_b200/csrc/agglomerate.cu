@@ -91,11 +91,19 @@ __global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bit
     }
 }
 
+// Flatten: every thread writes only its own entry, and only with a root, so
+// concurrent walks never see (or leave behind) a non-root written late. (A
+// path-halving find here would race: another thread could overwrite
+// parent[i] with a non-root ancestor after i stored its root.)
 __global__ void k_compress(u32* parent, const u64* n_sig_p) {
     const u64 n_sig = *n_sig_p;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
-         i += (u64)gridDim.x * blockDim.x)
-        parent[i] = uf_find(parent, (u32)i);
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 old = ld_parent(parent + i);
+        u32 r = old, next;
+        while (r > (next = ld_parent(parent + r))) r = next;
+        if (r != old) parent[i] = r;
+    }
 }
 
 // Per-root reductions. size/points start at 0, min_key at kEmpty.
