@@ -138,6 +138,7 @@ struct rg_ctx {
     Grid grid{};  // canvas packing (ingest)
     Grid res{};   // packing of the current significant set
     bool res_is_canvas = true;
+    bool narrow = false;  // canvas column/row indices fit int32 (K1 32-bit path)
     int device = 0;
     int n_sm = 148;
     int max_warps = 0;
@@ -275,7 +276,7 @@ rg_status validate(const rg_params* p, std::string& msg) {
     }
     const double cols = std::floor(p->x_max * s) - std::floor(p->x_min * s) + 1.0;
     const double rows = std::floor(p->y_max * s) - std::floor(p->y_min * s) + 1.0;
-    if (bits_for(cols) + bits_for(rows) > 63) {
+    if (bits_for(cols) + std::max<u32>(kBlockBits, bits_for(rows)) > 63) {
         msg = "canvas has too many tiles for a 63-bit packed tile key on the GPU path";
         return RG_ERR_UNSUPPORTED;
     }
@@ -294,17 +295,20 @@ Grid make_grid(const rg_params& p) {
     const double cols = std::floor(p.x_max * g.scale) - std::floor(p.x_min * g.scale) + 1.0;
     const double rows = std::floor(p.y_max * g.scale) - std::floor(p.y_min * g.scale) + 1.0;
     g.bits_x = bits_for(cols);
-    g.bits_y = bits_for(rows);
+    g.bits_y = std::max<u32>(kBlockBits, bits_for(rows));  // table blocks need >= 2 row bits
     return g;
 }
 
-Table table_of(const rg_ctx* c) {
+Table make_table(Slot* slots, u64 cap, u32 bits_y) {
     Table t;
-    t.slots = c->slots;
-    t.mask = c->cap - 1;
-    t.shift = 64 - log2u(c->cap);
+    t.slots = slots;
+    t.bmask = cap / kBucketSlots - 1;
+    t.shift = 64 - log2u(cap / kBucketSlots);
+    t.bits_y = bits_y;
     return t;
 }
+
+Table table_of(const rg_ctx* c) { return make_table(c->slots, c->cap, c->res.bits_y); }
 
 rg_status alloc_table(rg_ctx* ctx, u64 cap, Slot** out) {
     CK(dalloc(out, cap));
@@ -324,10 +328,7 @@ rg_status grow_table(rg_ctx* ctx, u64 new_cap) {
     rg_status s = alloc_table(ctx, new_cap, &ns);
     if (s != RG_OK) return s;
     if (ctx->slots) {
-        Table nt;
-        nt.slots = ns;
-        nt.mask = new_cap - 1;
-        nt.shift = 64 - log2u(new_cap);
+        const Table nt = make_table(ns, new_cap, ctx->res.bits_y);
         CK(launch_table_fold(ctx->slots, ctx->cap, nt, ctx->scratch, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
@@ -401,11 +402,15 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
     if (n == 0) return RG_OK;
     const u64 rows = (n + 31) / 32;
     const u64 w0 = (u64)ctx->max_warps;
+    const u64 batch = (u64)contract_batch_rows();
     u64 rps = rows / (8 * w0);
-    rps = std::max<u64>(4, std::min<u64>(64, rps));
+    rps = std::max<u64>(batch, std::min<u64>(64, rps)) / batch * batch;
     const u64 n_seg = (rows + rps - 1) / rps;
     const u64 W = std::min(w0, n_seg);
-    const u64 cap_min = next_pow2(107 * W + 1024);
+    // A warp checks its budget once per batch of rows, so it can overshoot
+    // by batch*32 - 1 keys: the table must hold soft + W*batch*32 keys, i.e.
+    // (1 - kMaxLoad) * cap > W * batch * 32.
+    const u64 cap_min = next_pow2((u64)((double)(W * batch * 32) / (1.0 - kMaxLoad)) + 1024);
 
     if (!ctx->slots) {
         u64 want;
@@ -451,6 +456,7 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
         L.n_partial_in = n_partial_in;
         L.partial_out = ctx->part[1 - pin];
         L.budget = (soft - ctx->used) / W;
+        L.narrow = ctx->narrow;
         CK(launch_contract(L, ctx->st));
         ++ctx->launches;
         rg_status s = pull_counters(ctx);
@@ -822,6 +828,13 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
     ctx->n_sm = prop.multiProcessorCount;
     ctx->grid = make_grid(*p);
     ctx->res = ctx->grid;
+    {
+        const double sc = ctx->grid.scale, lim = 2147483647.0;
+        const double c[4] = {std::floor(p->x_min * sc), std::floor(p->x_max * sc),
+                             std::floor(p->y_min * sc), std::floor(p->y_max * sc)};
+        ctx->narrow = true;
+        for (double v : c) ctx->narrow = ctx->narrow && v > -lim && v < lim;
+    }
     ctx->max_warps = contract_max_warps(ctx->n_sm);
     auto fail = [&](cudaError_t err, const char* what) {
         set_err(nullptr, err == cudaErrorMemoryAllocation ? RG_ERR_OOM : RG_ERR_CUDA,
@@ -1088,7 +1101,7 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     if (!on_canvas) {
         const double w = (double)mxx - (double)mnx + 1.0;
         const double h = (double)mxy - (double)mny + 1.0;
-        const u32 bx = bits_for(w), by = bits_for(h);
+        const u32 bx = bits_for(w), by = std::max<u32>(kBlockBits, bits_for(h));
         if (bx + by > 63)
             return set_err(ctx, RG_ERR_UNSUPPORTED,
                            "tile set spans too large a range for a 63-bit packed key");

@@ -35,13 +35,13 @@ namespace rg {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kCacheSlots = 128;
-constexpr int kBatch = 4;
+constexpr int kBatch = 4;  // rows per batch; the next batch is prefetched while one is processed
 
 struct K1Params {
     const double* xy;
     u64 n;
     u64 n_rows;
-    u64 rows_per_seg;
+    u64 rows_per_seg;  // multiple of kBatch
     u64 n_seg;
     Grid g;
     Table t;
@@ -49,38 +49,64 @@ struct K1Params {
     const Partial* partial_in;
     u64 n_partial_in;
     Partial* partial_out;
-    u64 budget;
+    u32 budget;  // per-warp bound on (claimed keys + cached entries)
 };
 
 __device__ __forceinline__ u32 cache_slot(u64 key) {
-    return (u32)((key * 0xD6E8FEB86659FD93ull) >> (64 - 7));
+    return (((u32)key ^ (u32)(key >> 32) * 0x85EBCA6Bu) * 0x9E3779B1u) >> 25;
 }
 
-template <bool kAligned>
-__device__ __forceinline__ void load_point(const double* xy, u64 idx, u64 n, u64 pol,
-                                           double& x, double& y) {
-    if (idx < n) {
-        if (kAligned) {
-            const double2 v = ld_point_stream(reinterpret_cast<const double2*>(xy) + idx, pol);
-            x = v.x;
-            y = v.y;
-        } else {
-            x = xy[2 * idx];
-            y = xy[2 * idx + 1];
-        }
+// Projection + packing; kNarrow when every canvas column/row index fits in
+// int32 (the host checks), so floor+convert is one cvt.rmi.s32.f64 and the
+// origin shift is 32-bit. Identical results to pack_key for such canvases.
+template <bool kNarrow>
+__device__ __forceinline__ u64 key_of(const Grid& g, double x, double y) {
+    if (kNarrow) {
+        const int tx = __double2int_rd(__dmul_rn(x, g.scale));
+        const int ty = __double2int_rd(__dmul_rn(y, g.scale));
+        const u32 kx = (u32)(tx - (int)g.origin_x);
+        const u32 ky = (u32)(ty - (int)g.origin_y);
+        return ((u64)kx << g.bits_y) | ky;
     } else {
-        x = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not in bounds
-        y = x;
+        return pack_key(g, x, y);
     }
 }
 
+struct Rows {
+    double x[kBatch], y[kBatch];
+};
+
+// Loads the lane's point of rows [r, r + kBatch) (rows >= row_end or indices
+// >= n become NaN, which fails the bounds test).
 template <bool kAligned>
+__device__ __forceinline__ void load_rows(const double* xy, u64 n, u64 r, u64 row_end, int lane,
+                                          u64 pol, Rows& o) {
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+        const u64 idx = (r + b) * 32 + lane;
+        if (r + b < row_end && idx < n) {
+            if (kAligned) {
+                const double2 v = ld_point_stream(reinterpret_cast<const double2*>(xy) + idx, pol);
+                o.x[b] = v.x;
+                o.y[b] = v.y;
+            } else {
+                o.x[b] = xy[2 * idx];
+                o.y[b] = xy[2 * idx + 1];
+            }
+        } else {
+            o.x[b] = o.y[b] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+}
+
+template <bool kAligned, bool kNarrow>
 __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
     __shared__ u64 s_key[kWarpsPerBlock][kCacheSlots];
     __shared__ u64 s_cnt[kWarpsPerBlock][kCacheSlots];
     __shared__ unsigned char s_owner[kWarpsPerBlock][kCacheSlots];
 
     const int lane = threadIdx.x & 31;
+    const u32 lane_bit = 1u << lane;
     const int wib = threadIdx.x >> 5;
     u64* ckey = s_key[wib];
     u64* ccnt = s_cnt[wib];
@@ -88,16 +114,18 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
     for (int i = lane; i < kCacheSlots; i += 32) ckey[i] = kEmpty;
     __syncwarp();
 
-    const Grid& g = P.g;
+    const Grid g = P.g;
     const u64 pol = evict_first_policy();
-    u64 claimed = 0;  // warp-uniform: keys this warp claimed in the table
-    u32 occ = 0;      // warp-uniform: occupied cache entries
-    u64 n_in = 0, n_out = 0;  // per lane
+    u32 pot = 0;          // warp-uniform: claimed keys + occupied cache entries
+    u32 claims = 0;       // per lane: keys this lane claimed in the table
+    u32 n_in = 0, n_out = 0;  // per lane
     bool stopped = false;
 
-    // Work queue: first the partial segments of a previous (stopped)
-    // launch, then fresh tickets.
-    auto fetch = [&](u64& seg, u64& row0) -> bool {
+    // Work queue: partial segments of a previous (stopped) launch first, then
+    // fresh tickets; the next ticket is requested while the current segment
+    // is processed.
+    u64 pending = ~0ull;  // prefetched ticket (lane 0's copy is authoritative)
+    auto fetch = [&](u64& seg, u64& row0, bool& from_ticket) -> bool {
         if (P.n_partial_in) {
             u64 pt = 0;
             if (lane == 0) pt = atomicAdd(&P.ctr->partial_ticket, 1ull);
@@ -105,15 +133,20 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
             if (pt < P.n_partial_in) {
                 seg = P.partial_in[pt].segment;
                 row0 = P.partial_in[pt].next_row;
+                from_ticket = false;
                 return true;
             }
         }
-        u64 t = 0;
-        if (lane == 0) t = atomicAdd(&P.ctr->ticket, 1ull);
+        u64 t = pending;
+        if (t == ~0ull) {
+            if (lane == 0) t = atomicAdd(&P.ctr->ticket, 1ull);
+        }
         t = __shfl_sync(kFull, t, 0);
+        pending = ~0ull;
         if (t >= P.n_seg) return false;
         seg = t;
         row0 = t * P.rows_per_seg;
+        from_ticket = true;
         return true;
     };
     auto record_partial = [&](u64 seg, u64 row) {
@@ -125,83 +158,92 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
     };
 
     u64 seg, row0;
-    bool have = fetch(seg, row0);
-    while (have && !stopped) {
+    bool from_ticket;
+    bool have = fetch(seg, row0, from_ticket);
+    while (have) {
         const u64 row_end = min((seg + 1) * P.rows_per_seg, P.n_rows);
+        // Prefetch the next ticket (only once the partial list is drained).
+        if (lane == 0 && (from_ticket || P.n_partial_in == 0)) pending = atomicAdd(&P.ctr->ticket, 1ull);
+        Rows cur, nxt;
+        load_rows<kAligned>(P.xy, P.n, row0, row_end, lane, pol, cur);
         for (u64 r = row0; r < row_end; r += kBatch) {
-            double xs[kBatch], ys[kBatch];
+            const u64 rn = r + kBatch;
+            if (rn < row_end) load_rows<kAligned>(P.xy, P.n, rn, row_end, lane, pol, nxt);
+            u64 key[kBatch];
+            bool inb[kBatch];
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) {
-                const u64 row = r + b;
-                const u64 idx = row * 32 + lane;
-                load_point<kAligned>(P.xy, row < row_end ? idx : P.n, P.n, pol, xs[b], ys[b]);
+                inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
+                const bool valid = (r + b < row_end) && ((r + b) * 32 + lane < P.n);
+                n_in += inb[b];
+                n_out += valid && !inb[b];
+                key[b] = inb[b] ? key_of<kNarrow>(g, cur.x[b], cur.y[b]) : kEmpty;
             }
+            u32 peers[kBatch];
+#pragma unroll
+            for (int b = 0; b < kBatch; ++b) peers[b] = __match_any_sync(kFull, key[b]);
+            u32 pot_lane = 0;
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) {
-                const u64 row = r + b;
-                if (row >= row_end) break;
-                const u64 idx = row * 32 + lane;
-                const bool valid = idx < P.n;
-                const bool inb = in_bounds(g, xs[b], ys[b]);
-                n_in += inb;
-                n_out += (valid && !inb);
-                const u64 key = inb ? pack_key(g, xs[b], ys[b]) : kEmpty;
-                const u32 peers = __match_any_sync(kFull, key);
-                const bool leader = inb && (lane == __ffs(peers) - 1);
-                const u32 cs = cache_slot(key);
+                const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
+                const u32 cs = cache_slot(key[b]);
                 if (leader) owner[cs] = (unsigned char)lane;
                 __syncwarp();
-                u32 delta = 0;  // low 16: claimed keys, high 16: new cache entries
                 if (leader) {
-                    const u64 cnt = __popc(peers);
+                    const u64 cnt = __popc(peers[b]);
                     if (owner[cs] == lane) {
                         const u64 ek = ckey[cs];
-                        if (ek == key) {
+                        if (ek == key[b]) {
                             ccnt[cs] += cnt;
                         } else {
                             if (ek != kEmpty) {
-                                delta += table_add(P.t, ek, ccnt[cs]) ? 1u : 0u;
+                                const u32 c = table_add(P.t, ek, ccnt[cs]) ? 1u : 0u;
+                                claims += c;
+                                pot_lane += c;
                             } else {
-                                delta += 1u << 16;
+                                pot_lane += 1;  // a new occupied cache entry
                             }
-                            ckey[cs] = key;
+                            ckey[cs] = key[b];
                             ccnt[cs] = cnt;
                         }
                     } else {
-                        delta += table_add(P.t, key, cnt) ? 1u : 0u;
+                        const u32 c = table_add(P.t, key[b], cnt) ? 1u : 0u;
+                        claims += c;
+                        pot_lane += c;
                     }
                 }
                 __syncwarp();
-                const u32 sum = __reduce_add_sync(kFull, delta);
-                claimed += sum & 0xffffu;
-                occ += sum >> 16;
-                if (claimed + occ >= P.budget) {
-                    // Out of budget: hand the rest of this segment back.
-                    if (row + 1 < row_end) record_partial(seg, row + 1);
-                    stopped = true;
-                    break;
-                }
             }
-            if (stopped) break;
+            pot += __reduce_add_sync(kFull, pot_lane);
+            if (pot >= P.budget) {
+                // Out of budget: hand back the rest of this segment and the
+                // prefetched ticket.
+                if (rn < row_end) record_partial(seg, rn);
+                const u64 t = __shfl_sync(kFull, pending, 0);
+                if (t != ~0ull && t < P.n_seg) record_partial(t, t * P.rows_per_seg);
+                stopped = true;
+                break;
+            }
+            cur = nxt;
         }
-        if (!stopped) have = fetch(seg, row0);
+        if (stopped) break;
+        have = fetch(seg, row0, from_ticket);
     }
 
     // Write back the cache.
-    u32 fl = 0;
     for (int i = lane; i < kCacheSlots; i += 32) {
         const u64 k = ckey[i];
-        if (k != kEmpty) fl += table_add(P.t, k, ccnt[i]) ? 1u : 0u;
+        if (k != kEmpty) claims += table_add(P.t, k, ccnt[i]) ? 1u : 0u;
     }
-    claimed += __reduce_add_sync(kFull, fl);
 
     // Counters: one atomic per warp.
-    const u64 wi = __reduce_add_sync(kFull, (u32)n_in);  // < 2^32 per warp per launch
-    const u64 wo = __reduce_add_sync(kFull, (u32)n_out);
+    const u32 wc = __reduce_add_sync(kFull, claims);
+    const u32 wi = __reduce_add_sync(kFull, n_in);
+    const u32 wo = __reduce_add_sync(kFull, n_out);
     if (lane == 0) {
-        if (wi) atomicAdd(&P.ctr->ingested, wi);
-        if (wo) atomicAdd(&P.ctr->skipped, wo);
-        if (claimed) atomicAdd(&P.ctr->used, claimed);
+        if (wi) atomicAdd(&P.ctr->ingested, (u64)wi);
+        if (wo) atomicAdd(&P.ctr->skipped, (u64)wo);
+        if (wc) atomicAdd(&P.ctr->used, (u64)wc);
         if (stopped) atomicAdd(&P.ctr->stopped, 1ull);
     }
 }
@@ -245,54 +287,49 @@ __global__ void k_first_oob(const double* xy, u64 n, Grid g, u64* first) {
 }
 
 // K2: TileAccumulator::prune accumulator.hpp:160-174 — keep count >= tau.
-// Each significant slot gets a dense index (block-aggregated append), its
-// key/count are written to the compact arrays, the slot's value word becomes
-// SIG_BIT | index and the union-find parent is initialised.
-constexpr int kK2Items = 4;
+// Each significant slot gets a dense index, its key/count are written to the
+// compact arrays, the slot's value word becomes SIG_BIT | index and the
+// union-find parent is initialised. A warp owns 32 x kK2Items consecutive
+// slots (coalesced 16-byte loads, all issued before any use) and reserves its
+// output range with one atomic; no block-wide barrier sits on the path, so
+// the atomic's round trip overlaps other warps' loads.
+constexpr int kK2Items = 8;
 __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, u64* sig_key,
                                                  u64* sig_cnt, u32* parent, Counters* ctr) {
-    __shared__ u32 s_warp[8];
-    __shared__ u64 s_base;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const u64 per_block = 256ull * kK2Items;
-    for (u64 base = blockIdx.x * per_block; base < cap; base += (u64)gridDim.x * per_block) {
+    const int lane = threadIdx.x & 31;
+    const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+    const u64 n_warps = ((u64)gridDim.x * blockDim.x) >> 5;
+    constexpr u64 per_warp = 32ull * kK2Items;
+    for (u64 base = warp * per_warp; base < cap; base += n_warps * per_warp) {
         u64 k[kK2Items], v[kK2Items];
-        u32 nsig = 0;
 #pragma unroll
         for (int j = 0; j < kK2Items; ++j) {
-            const u64 i = base + j * 256 + threadIdx.x;
+            const u64 i = base + j * 32 + lane;
             if (i < cap) {
                 ld_slot(t.slots + i, k[j], v[j]);
             } else {
                 k[j] = kEmpty;
                 v[j] = 0;
             }
-            nsig += (k[j] != kEmpty && v[j] >= tau);
         }
-        // block-exclusive scan of nsig
+        u32 nsig = 0;
+#pragma unroll
+        for (int j = 0; j < kK2Items; ++j) nsig += (k[j] != kEmpty && v[j] >= tau);
         u32 incl = nsig;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const u32 y = __shfl_up_sync(kFull, incl, o);
             if (lane >= o) incl += y;
         }
-        if (lane == 31) s_warp[wib] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            u32 tot = 0;
-            for (int w = 0; w < 8; ++w) {
-                const u32 c = s_warp[w];
-                s_warp[w] = tot;
-                tot += c;
-            }
-            s_base = tot ? atomicAdd(&ctr->n_sig, (u64)tot) : 0;
-        }
-        __syncthreads();
-        u64 pos = s_base + s_warp[wib] + incl - nsig;
+        const u32 total = __shfl_sync(kFull, incl, 31);
+        if (total == 0) continue;
+        u64 at = 0;
+        if (lane == 31) at = atomicAdd(&ctr->n_sig, (u64)total);
+        u64 pos = __shfl_sync(kFull, at, 31) + incl - nsig;
 #pragma unroll
         for (int j = 0; j < kK2Items; ++j) {
             if (k[j] != kEmpty && v[j] >= tau) {
-                const u64 i = base + j * 256 + threadIdx.x;
+                const u64 i = base + j * 32 + lane;
                 sig_key[pos] = k[j];
                 sig_cnt[pos] = v[j];
                 parent[pos] = (u32)pos;
@@ -300,25 +337,31 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, u64*
                 ++pos;
             }
         }
-        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------- launchers
 
-static int g_k1_blocks_per_sm[2] = {0, 0};
+static int g_k1_warps_per_sm = 0;
 
+// Resident warps per SM of the slowest K1 variant: the launch is persistent
+// (one wave), and the per-warp new-key budget bounds how far the table can
+// overshoot its load target (see ingest_device in api.cu).
 int contract_max_warps(int n_sm) {
-    if (!g_k1_blocks_per_sm[1]) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k1_blocks_per_sm[1], k_contract<true>,
-                                                      kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k1_blocks_per_sm[0], k_contract<false>,
-                                                      kThreads, 0);
-        if (g_k1_blocks_per_sm[1] < 1) g_k1_blocks_per_sm[1] = 1;
-        if (g_k1_blocks_per_sm[0] < 1) g_k1_blocks_per_sm[0] = 1;
+    if (!g_k1_warps_per_sm) {
+        int b[4] = {0, 0, 0, 0};
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_contract<true, true>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_contract<true, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_contract<false, true>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_contract<false, false>, kThreads, 0);
+        int m = b[0];
+        for (int i = 1; i < 4; ++i) m = b[i] < m ? b[i] : m;
+        g_k1_warps_per_sm = (m < 1 ? 1 : m) * kWarpsPerBlock;
     }
-    return g_k1_blocks_per_sm[1] * n_sm * kWarpsPerBlock;
+    return g_k1_warps_per_sm * n_sm;
 }
+
+int contract_batch_rows() { return kBatch; }
 
 cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     K1Params P;
@@ -333,13 +376,17 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     P.partial_in = L.partial_in;
     P.n_partial_in = L.n_partial_in;
     P.partial_out = L.partial_out;
-    P.budget = L.budget;
+    P.budget = (u32)(L.budget < (1ull << 30) ? L.budget : (1ull << 30));
     const int blocks = (int)((L.warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const bool aligned = ((uintptr_t)L.xy & 15) == 0;
-    if (aligned)
-        k_contract<true><<<blocks, kThreads, 0, st>>>(P);
+    if (aligned && L.narrow)
+        k_contract<true, true><<<blocks, kThreads, 0, st>>>(P);
+    else if (aligned)
+        k_contract<true, false><<<blocks, kThreads, 0, st>>>(P);
+    else if (L.narrow)
+        k_contract<false, true><<<blocks, kThreads, 0, st>>>(P);
     else
-        k_contract<false><<<blocks, kThreads, 0, st>>>(P);
+        k_contract<false, false><<<blocks, kThreads, 0, st>>>(P);
     return cudaGetLastError();
 }
 
@@ -370,7 +417,7 @@ cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt
                            Counters* ctr, int n_sm, cudaStream_t st) {
     const u64 per_block = 256ull * kK2Items;
     const u64 want = (cap + per_block - 1) / per_block;
-    const int blocks = (int)(want < (u64)n_sm * 8 ? (want ? want : 1) : (u64)n_sm * 8);
+    const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, sig_key, sig_cnt, parent, ctr);
     return cudaGetLastError();
 }

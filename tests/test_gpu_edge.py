@@ -112,8 +112,11 @@ def test_unaligned_device_pointer():
 
 @pytest.mark.parametrize("hint", [1, 1000])
 def test_tiny_table_grows_exactly(hint):
-    pts = D.generate(D.spec(2, 0.3), shuffle_seed=1)  # ~3M points, ~400K tiles
-    gp = D.params(2)
+    s = D.spec(2, 0.3)
+    s.n_noise = 4_000_000  # ~4M distinct tiles at p=3: far above the initial table
+    pts = D.generate(s, shuffle_seed=1)
+    gp = D.params(3)
+    gp.threshold = 1
     gp.capacity_hint = hint
     pl = Pipeline(gp)
     st = pl.run(pts)
