@@ -75,9 +75,16 @@ __global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bit
     const u64 n_sig = *n_sig_p;
     const long long ymask = (1ll << bits_y) - 1;
     const long long xlim = 1ll << bits_x, ylim = 1ll << bits_y;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+    // Compaction emits tiles bucket by bucket, so consecutive indices are
+    // spatial neighbours of one cluster. Giving the 32 lanes of a warp tiles
+    // n/32 apart keeps their union CASes on different roots (no intra-warp
+    // contention); each lane's own neighbour probes still hit its bucket.
+    const u64 chunk = (n_sig + 31) / 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < 32 * chunk;
          i += (u64)gridDim.x * blockDim.x) {
-        const u64 key = sig_key[i];
+        const u64 idx = (i & 31) * chunk + (i >> 5);
+        if (idx >= n_sig) continue;
+        const u64 key = sig_key[idx];
         const long long kx = (long long)(key >> bits_y);
         const long long ky = (long long)key & ymask;
         for (int o = 0; o < off.n; ++o) {
@@ -86,7 +93,7 @@ __global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bit
             if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) continue;
             const u64 nkey = ((u64)nx << bits_y) | (u64)ny;
             const u64 v = table_find(t, nkey);
-            if (v != kEmpty && (v & kSigBit)) uf_unite(parent, (u32)i, (u32)(v & ~kSigBit));
+            if (v != kEmpty && (v & kSigBit)) uf_unite(parent, (u32)idx, (u32)(v & ~kSigBit));
         }
     }
 }
@@ -106,16 +113,43 @@ __global__ void k_compress(u32* parent, const u64* n_sig_p) {
     }
 }
 
-// Per-root reductions. size/points start at 0, min_key at kEmpty.
+// Per-root reductions (size/points start at 0, min_key at kEmpty). Tiles of
+// one component sit in runs of consecutive indices (compaction order is
+// bucket order), so each warp first reduces its contiguous runs with a
+// segmented shuffle reduction and only run heads touch global memory.
 __global__ void k_root_reduce(const u32* parent, const u64* sig_key, const u64* sig_cnt,
                               const u64* n_sig_p, u32* size, u64* npts, u64* min_key) {
     const u64 n_sig = *n_sig_p;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
+    const int lane = threadIdx.x & 31;
+    const u64 span = ((n_sig + 31) / 32) * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
-        const u32 r = parent[i];
-        atomicAdd(size + r, 1u);
-        atomicAdd(npts + r, sig_cnt ? sig_cnt[i] : 0ull);
-        atomicMin(min_key + r, sig_key[i]);
+        const bool valid = i < n_sig;
+        const u32 r = valid ? parent[i] : 0xffffffffu;
+        u32 cnt = valid ? 1u : 0u;
+        u64 pts = valid && sig_cnt ? sig_cnt[i] : 0ull;
+        u64 mk = valid ? sig_key[i] : kEmpty;
+        const u32 prev = __shfl_up_sync(kFull, r, 1);
+        const bool head = lane == 0 || prev != r;
+        const u32 heads = __ballot_sync(kFull, head);
+        const u32 run = __popc(heads & (0xffffffffu >> (31 - lane)));  // 1-based run id
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 orun = __shfl_down_sync(kFull, run, o);
+            const u32 oc = __shfl_down_sync(kFull, cnt, o);
+            const u64 op = __shfl_down_sync(kFull, pts, o);
+            const u64 om = __shfl_down_sync(kFull, mk, o);
+            if (lane + o < 32 && orun == run) {
+                cnt += oc;
+                pts += op;
+                mk = om < mk ? om : mk;
+            }
+        }
+        if (head && valid) {
+            atomicAdd(size + r, cnt);
+            atomicAdd(npts + r, pts);
+            atomicMin(min_key + r, mk);
+        }
     }
 }
 

@@ -406,7 +406,7 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
     u64 rps = rows / (8 * w0);
     rps = std::max<u64>(batch, std::min<u64>(64, rps)) / batch * batch;
     const u64 n_seg = (rows + rps - 1) / rps;
-    const u64 W = std::min(w0, n_seg);
+    const u64 W = (std::min(w0, n_seg) + 7) / 8 * 8;  // whole blocks of 8 warps (w0 is a multiple of 8)
     // A warp checks its budget once per batch of rows, so it can overshoot
     // by batch*32 - 1 keys: the table must hold soft + W*batch*32 keys, i.e.
     // (1 - kMaxLoad) * cap > W * batch * 32.
@@ -863,7 +863,7 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
     if ((e = cudaMemset(ctx->ctr, 0, sizeof(Counters))) != cudaSuccess)
         return fail(e, "cudaMemset");
     for (int b = 0; b < 2; ++b)
-        if ((e = dalloc(&ctx->part[b], (u64)ctx->max_warps)) != cudaSuccess)
+        if ((e = dalloc(&ctx->part[b], 2 * (u64)ctx->max_warps + 64)) != cudaSuccess)  // <= 2 per warp
             return fail(e, "cudaMalloc partials");
     if ((e = dalloc(&ctx->scratch, 8)) != cudaSuccess) return fail(e, "cudaMalloc scratch");
     const std::vector<int2> off = forward_offsets(*p);
@@ -1123,6 +1123,7 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
         if (s != RG_OK) return s;
         ctx->cap = need;
     }
+    ctx->res = res;  // the table is keyed with this packing
     s = ensure_sig_capacity(ctx, n);
     if (s != RG_OK) return s;
     if (n) {

@@ -1,0 +1,28 @@
+"""Diagnostic: where does the end-to-end (host-buffer) time go?"""
+import sys, time
+sys.path.insert(0, '.')
+import numpy as np, torch
+from paper_1907_03620_b200 import datagen as D, _native as N
+from paper_1907_03620_b200.raster import Pipeline
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+s = D.spec(cfg); n = D.count(s); gp = D.params(cfg)
+host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+D.generate_into(s, host.data_ptr())
+dev = host.cuda()
+pl = Pipeline(gp)
+for _ in range(2):
+    pl.run(dev)
+torch.cuda.synchronize()
+def t(f, k=3):
+    out = []
+    for _ in range(k):
+        torch.cuda.synchronize(); a = time.perf_counter(); f(); torch.cuda.synchronize(); out.append(time.perf_counter() - a)
+    return min(out) * 1e3
+print('device run ms', t(lambda: pl.run(dev)))
+print('host run ms', t(lambda: pl.run(host)))
+st = pl.ctx.stats()
+S = st.n_significant
+tx = np.empty(S, np.int64); ty = np.empty(S, np.int64); cnt = np.empty(S, np.uint64); cid = np.empty(S, np.int64)
+print('get_significant ms', t(lambda: pl.ctx.lib.rg_get_significant(pl.ctx.h, tx.ctypes.data, ty.ctypes.data, cnt.ctypes.data, cid.ctypes.data, S, N.RG_MEM_HOST)))
+print('torch h2d 8GB ms', t(lambda: dev.copy_(host, non_blocking=True)))
