@@ -76,22 +76,24 @@ struct Rows {
     double x[kBatch], y[kBatch];
 };
 
-// Loads the lane's point of rows [r, r + kBatch) (rows >= row_end or indices
-// >= n become NaN, which fails the bounds test).
+// Loads the lane's point of the kBatch rows starting at point index p0
+// (p0 = first point of the batch; `left` = valid points in the batch, <=
+// 32*kBatch). Missing points become NaN, which fails the bounds test.
 template <bool kAligned>
-__device__ __forceinline__ void load_rows(const double* xy, u64 n, u64 r, u64 row_end, int lane,
-                                          u64 pol, Rows& o) {
+__device__ __forceinline__ void load_rows(const double* xy, u64 p0, u32 left, int lane, u64 pol,
+                                          Rows& o) {
+    const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-        const u64 idx = (r + b) * 32 + lane;
-        if (r + b < row_end && idx < n) {
+        if ((u32)(b * 32 + lane) < left) {
             if (kAligned) {
-                const double2 v = ld_point_stream(reinterpret_cast<const double2*>(xy) + idx, pol);
+                const double2 v = ld_point_stream(base + b * 32, pol);
                 o.x[b] = v.x;
                 o.y[b] = v.y;
             } else {
-                o.x[b] = xy[2 * idx];
-                o.y[b] = xy[2 * idx + 1];
+                const double* q = xy + 2 * (p0 + b * 32 + lane);
+                o.x[b] = q[0];
+                o.y[b] = q[1];
             }
         } else {
             o.x[b] = o.y[b] = __longlong_as_double(0x7ff8000000000000ll);
@@ -100,7 +102,7 @@ __device__ __forceinline__ void load_rows(const double* xy, u64 n, u64 r, u64 ro
 }
 
 template <bool kAligned, bool kNarrow>
-__global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
+__global__ void __launch_bounds__(kThreads, 4) k_contract(K1Params P) {
     __shared__ u64 s_key[kWarpsPerBlock][kCacheSlots];
     __shared__ u64 s_cnt[kWarpsPerBlock][kCacheSlots];
     __shared__ unsigned char s_owner[kWarpsPerBlock][kCacheSlots];
@@ -116,9 +118,10 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
 
     const Grid g = P.g;
     const u64 pol = evict_first_policy();
-    u32 pot = 0;          // warp-uniform: claimed keys + occupied cache entries
-    u32 claims = 0;       // per lane: keys this lane claimed in the table
-    u32 n_in = 0, n_out = 0;  // per lane
+    u32 pot = 0;      // warp-uniform: claimed keys + occupied cache entries
+    u32 claims = 0;   // per lane: keys this lane claimed in the table
+    u32 n_in = 0;     // per lane: in-bounds points
+    u64 n_valid = 0;  // warp-uniform: points examined
     bool stopped = false;
 
     // Work queue: partial segments of a previous (stopped) launch first, then
@@ -162,40 +165,54 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
     bool have = fetch(seg, row0, from_ticket);
     while (have) {
         const u64 row_end = min((seg + 1) * P.rows_per_seg, P.n_rows);
-        // Prefetch the next ticket (only once the partial list is drained).
-        if (lane == 0 && (from_ticket || P.n_partial_in == 0)) pending = atomicAdd(&P.ctr->ticket, 1ull);
+        const u64 p_end = min(row_end * 32, P.n);
+        if (lane == 0 && (from_ticket || P.n_partial_in == 0))
+            pending = atomicAdd(&P.ctr->ticket, 1ull);
         Rows cur, nxt;
-        load_rows<kAligned>(P.xy, P.n, row0, row_end, lane, pol, cur);
-        for (u64 r = row0; r < row_end; r += kBatch) {
-            const u64 rn = r + kBatch;
-            if (rn < row_end) load_rows<kAligned>(P.xy, P.n, rn, row_end, lane, pol, nxt);
+        u64 p0 = row0 * 32;
+        u32 left = (u32)min(p_end - p0, (u64)(32 * kBatch));
+        load_rows<kAligned>(P.xy, p0, left, lane, pol, cur);
+        while (true) {
+            const u64 pn = p0 + 32 * kBatch;
+            const u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
+            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, nxt);
+            n_valid += left;
+
             u64 key[kBatch];
             bool inb[kBatch];
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) {
                 inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
-                const bool valid = (r + b < row_end) && ((r + b) * 32 + lane < P.n);
                 n_in += inb[b];
-                n_out += valid && !inb[b];
                 key[b] = inb[b] ? key_of<kNarrow>(g, cur.x[b], cur.y[b]) : kEmpty;
             }
             u32 peers[kBatch];
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) peers[b] = __match_any_sync(kFull, key[b]);
+
             u32 pot_lane = 0;
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) {
                 const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
                 const u32 cs = cache_slot(key[b]);
-                if (leader) owner[cs] = (unsigned char)lane;
-                __syncwarp();
+                // Hits: the slot already holds this key; distinct keys never
+                // hit the same slot, so leaders add without arbitration.
+                bool miss = false;
                 if (leader) {
-                    const u64 cnt = __popc(peers[b]);
-                    if (owner[cs] == lane) {
-                        const u64 ek = ckey[cs];
-                        if (ek == key[b]) {
-                            ccnt[cs] += cnt;
-                        } else {
+                    if (ckey[cs] == key[b])
+                        ccnt[cs] += __popc(peers[b]);
+                    else
+                        miss = true;
+                }
+                if (__any_sync(kFull, miss)) {
+                    // Misses: one leader per slot installs its key (flushing
+                    // the previous occupant to HBM); the rest go to HBM.
+                    if (miss) owner[cs] = (unsigned char)lane;
+                    __syncwarp();
+                    if (miss) {
+                        const u64 cnt = __popc(peers[b]);
+                        if (owner[cs] == lane) {
+                            const u64 ek = ckey[cs];
                             if (ek != kEmpty) {
                                 const u32 c = table_add(P.t, ek, ccnt[cs]) ? 1u : 0u;
                                 claims += c;
@@ -205,11 +222,11 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
                             }
                             ckey[cs] = key[b];
                             ccnt[cs] = cnt;
+                        } else {
+                            const u32 c = table_add(P.t, key[b], cnt) ? 1u : 0u;
+                            claims += c;
+                            pot_lane += c;
                         }
-                    } else {
-                        const u32 c = table_add(P.t, key[b], cnt) ? 1u : 0u;
-                        claims += c;
-                        pot_lane += c;
                     }
                 }
                 __syncwarp();
@@ -218,13 +235,16 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
             if (pot >= P.budget) {
                 // Out of budget: hand back the rest of this segment and the
                 // prefetched ticket.
-                if (rn < row_end) record_partial(seg, rn);
+                if (left_n) record_partial(seg, pn / 32);
                 const u64 t = __shfl_sync(kFull, pending, 0);
                 if (t != ~0ull && t < P.n_seg) record_partial(t, t * P.rows_per_seg);
                 stopped = true;
                 break;
             }
+            if (!left_n) break;
             cur = nxt;
+            p0 = pn;
+            left = left_n;
         }
         if (stopped) break;
         have = fetch(seg, row0, from_ticket);
@@ -238,11 +258,10 @@ __global__ void __launch_bounds__(kThreads) k_contract(K1Params P) {
 
     // Counters: one atomic per warp.
     const u32 wc = __reduce_add_sync(kFull, claims);
-    const u32 wi = __reduce_add_sync(kFull, n_in);
-    const u32 wo = __reduce_add_sync(kFull, n_out);
+    const u64 wi = __reduce_add_sync(kFull, n_in);
     if (lane == 0) {
-        if (wi) atomicAdd(&P.ctr->ingested, (u64)wi);
-        if (wo) atomicAdd(&P.ctr->skipped, (u64)wo);
+        if (wi) atomicAdd(&P.ctr->ingested, wi);
+        if (n_valid > wi) atomicAdd(&P.ctr->skipped, n_valid - wi);
         if (wc) atomicAdd(&P.ctr->used, (u64)wc);
         if (stopped) atomicAdd(&P.ctr->stopped, 1ull);
     }
