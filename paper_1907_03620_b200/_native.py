@@ -157,7 +157,10 @@ def gpu():
     """The sm_100a clustering library (product path)."""
     global _gpu
     if _gpu is None:
-        _gpu = _load(GPU_LIB, GPU_SYMBOLS, "libraster_b200.so")
+        import os
+
+        override = os.environ.get("RASTER_B200_LIB")  # A/B experiments with variant builds
+        _gpu = _load(Path(override) if override else GPU_LIB, GPU_SYMBOLS, "libraster_b200.so")
     return _gpu
 
 

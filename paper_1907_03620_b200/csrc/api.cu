@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -20,6 +21,7 @@ using namespace rg;
 namespace {
 
 thread_local std::string g_create_error;
+const bool g_debug = std::getenv("RG_DEBUG") != nullptr;
 
 constexpr double kMaxLoad = 0.7;  // TileCounts grows at 70% load (accumulator.hpp:34)
 constexpr u64 kStagePoints = 1ull << 24;  // 256 MB per staging buffer
@@ -461,10 +463,30 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
         ++ctx->launches;
         rg_status s = pull_counters(ctx);
         if (s != RG_OK) return s;
+        if (g_debug)
+            std::fprintf(stderr,
+                         "[rg] ingest n=%llu round=%d W=%llu rps=%llu cap=%llu used=%llu budget=%llu "
+                         "stopped=%llu partial=%llu ticket=%llu n_in_partial=%llu ingested=%llu\n",
+                         (unsigned long long)n, round, (unsigned long long)W, (unsigned long long)rps,
+                         (unsigned long long)ctx->cap, (unsigned long long)ctx->used,
+                         (unsigned long long)L.budget, (unsigned long long)ctx->hctr->stopped,
+                         (unsigned long long)ctx->hctr->n_partial,
+                         (unsigned long long)ctx->hctr->ticket, (unsigned long long)n_partial_in,
+                         (unsigned long long)ctx->ingested);
         if (ctx->hctr->stopped == 0) break;
         // Some warps ran out of budget: resume their partial segments (and
         // the untouched tickets) after growing if the table is filling up.
-        n_partial_in = ctx->hctr->n_partial;
+        // Partial segments of the previous round that no warp reached before
+        // every warp ran out of budget are carried over behind the new ones.
+        const u64 taken = std::min<u64>(ctx->hctr->partial_ticket, n_partial_in);
+        u64 n_next = ctx->hctr->n_partial;
+        if (taken < n_partial_in) {
+            CK(cudaMemcpyAsync(ctx->part[1 - pin] + n_next, ctx->part[pin] + taken,
+                               (n_partial_in - taken) * sizeof(Partial), cudaMemcpyDeviceToDevice,
+                               ctx->st));
+            n_next += n_partial_in - taken;
+        }
+        n_partial_in = n_next;
         pin = 1 - pin;
         zero_field(ctx, &ctx->ctr->n_partial);
         zero_field(ctx, &ctx->ctr->partial_ticket);

@@ -54,7 +54,10 @@ struct Grid {
     u32 bits_x;
 };
 
-constexpr u32 kBlockBits = 2;                  // 4x4-tile blocks
+#ifndef RG_BLOCK_BITS
+#define RG_BLOCK_BITS 2
+#endif
+constexpr u32 kBlockBits = RG_BLOCK_BITS;       // 2: 4x4-tile blocks
 constexpr u32 kBucketSlots = 1u << (2 * kBlockBits);  // 16 slots per bucket
 
 struct Table {

@@ -35,7 +35,13 @@ namespace rg {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kCacheSlots = 128;
-constexpr int kBatch = 4;  // rows per batch; the next batch is prefetched while one is processed
+#ifndef RG_K1_BATCH
+#define RG_K1_BATCH 4
+#endif
+#ifndef RG_K1_MINBLOCKS
+#define RG_K1_MINBLOCKS 4
+#endif
+constexpr int kBatch = RG_K1_BATCH;  // rows per batch; the next batch is prefetched while one is processed
 
 struct K1Params {
     const double* xy;
@@ -52,9 +58,19 @@ struct K1Params {
     u32 budget;  // per-warp bound on (claimed keys + cached entries)
 };
 
-__device__ __forceinline__ u32 cache_slot(u64 key) {
+// Cache slot of a tile: direct-mapped by position in an 8 x 16-tile window
+// (low 3 column bits, low 4 row bits), so the tiles of one cluster (a few
+// tiles across) never evict each other; keys of unrelated regions are spread
+// by their low coordinate bits.
+#ifndef RG_CACHE_HASH
+__device__ __forceinline__ u32 cache_slot(u64 key, u32 bits_y) {
+    return (((u32)(key >> bits_y) & 7u) << 4) | ((u32)key & 15u);
+}
+#else
+__device__ __forceinline__ u32 cache_slot(u64 key, u32) {
     return (((u32)key ^ (u32)(key >> 32) * 0x85EBCA6Bu) * 0x9E3779B1u) >> 25;
 }
+#endif
 
 // Projection + packing; kNarrow when every canvas column/row index fits in
 // int32 (the host checks), so floor+convert is one cvt.rmi.s32.f64 and the
@@ -102,7 +118,7 @@ __device__ __forceinline__ void load_rows(const double* xy, u64 p0, u32 left, in
 }
 
 template <bool kAligned, bool kNarrow>
-__global__ void __launch_bounds__(kThreads, 4) k_contract(K1Params P) {
+__global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ u64 s_key[kWarpsPerBlock][kCacheSlots];
     __shared__ u64 s_cnt[kWarpsPerBlock][kCacheSlots];
     __shared__ unsigned char s_owner[kWarpsPerBlock][kCacheSlots];
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_contract(K1Params P) {
 #pragma unroll
             for (int b = 0; b < kBatch; ++b) {
                 const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
-                const u32 cs = cache_slot(key[b]);
+                const u32 cs = cache_slot(key[b], g.bits_y);
                 // Hits: the slot already holds this key; distinct keys never
                 // hit the same slot, so leaders add without arbitration.
                 bool miss = false;
