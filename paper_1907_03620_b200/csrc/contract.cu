@@ -36,7 +36,7 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kCacheSlots = 128;
 #ifndef RG_K1_BATCH
-#define RG_K1_BATCH 4
+#define RG_K1_BATCH 2
 #endif
 #ifndef RG_K1_MINBLOCKS
 #define RG_K1_MINBLOCKS 4
@@ -117,26 +117,113 @@ __device__ __forceinline__ void load_rows(const double* xy, u64 p0, u32 left, in
     }
 }
 
+// Per-warp shared state of K1.
+struct WarpSmem {
+    u64 ckey[kCacheSlots];   // direct-mapped write-back cache: keys
+    u64 ccnt[kCacheSlots];   //                                 counts
+    u64 skey[64];            // staged (key, count) pairs bound for the HBM table
+    u64 scnt[64];
+    unsigned char owner[kCacheSlots];
+};
+
+struct K1State {
+    u32 pot;      // warp-uniform: claimed keys + occupied cache entries + staged entries
+    u32 slen;     // warp-uniform: staged entries
+    u32 claims;   // per lane: keys this lane claimed in the table
+    u32 n_in;     // per lane: in-bounds points
+};
+
+// Flush the staging list with every lane active: one table_add per entry,
+// lanes in parallel (the divergent, latency-bound part of a miss is paid
+// once per 32 misses instead of once per row).
+__device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State& s, int lane) {
+    u32 c = 0;
+    for (u32 e = lane; e < s.slen; e += 32) c += table_add(t, w.skey[e], w.scnt[e]) ? 1u : 0u;
+    const u32 claimed = __reduce_add_sync(kFull, c);
+    s.claims += c;
+    s.pot = s.pot - s.slen + claimed;
+    s.slen = 0;
+    __syncwarp();
+}
+
+// One batch of kBatch rows already in registers.
+template <bool kNarrow>
+__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const Rows& cur,
+                                              WarpSmem& w, K1State& s, int lane, u32 lane_bit,
+                                              u32 lt_mask) {
+    u64 key[kBatch];
+    bool inb[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+        inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
+        s.n_in += inb[b];
+        key[b] = inb[b] ? key_of<kNarrow>(g, cur.x[b], cur.y[b]) : kEmpty;
+    }
+    u32 peers[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) peers[b] = __match_any_sync(kFull, key[b]);
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+        const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
+        const u32 cs = cache_slot(key[b], g.bits_y);
+        const u64 cnt = __popc(peers[b]);
+        // Hit: the slot holds this key. Distinct keys never hit the same
+        // slot, so hitting leaders add without arbitration.
+        bool miss = false;
+        if (leader) {
+            if (w.ckey[cs] == key[b])
+                w.ccnt[cs] += cnt;
+            else
+                miss = true;
+        }
+        const u32 missmask = __ballot_sync(kFull, miss);
+        if (missmask) {
+            // One missing leader per slot installs its key; the slot's old
+            // occupant (if any) and the other missing leaders are staged.
+            if (miss) w.owner[cs] = (unsigned char)lane;
+            __syncwarp();
+            const bool win = miss && w.owner[cs] == lane;
+            u64 sk = key[b], sc = cnt;
+            bool was_empty = false;
+            if (win) {
+                sk = w.ckey[cs];
+                sc = w.ccnt[cs];
+                was_empty = sk == kEmpty;
+                w.ckey[cs] = key[b];
+                w.ccnt[cs] = cnt;
+            }
+            const bool stage = miss && !was_empty;
+            const u32 smask = __ballot_sync(kFull, stage);
+            const u32 emask = __ballot_sync(kFull, was_empty);
+            if (stage) {
+                const u32 pos = s.slen + __popc(smask & lt_mask);
+                w.skey[pos] = sk;
+                w.scnt[pos] = sc;
+            }
+            s.slen += __popc(smask);
+            s.pot += __popc(smask) + __popc(emask);
+            __syncwarp();
+            if (s.slen >= 32) flush_stage(t, w, s, lane);
+        }
+        __syncwarp();
+    }
+}
+
 template <bool kAligned, bool kNarrow>
 __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
-    __shared__ u64 s_key[kWarpsPerBlock][kCacheSlots];
-    __shared__ u64 s_cnt[kWarpsPerBlock][kCacheSlots];
-    __shared__ unsigned char s_owner[kWarpsPerBlock][kCacheSlots];
+    __shared__ WarpSmem s_warp[kWarpsPerBlock];
 
     const int lane = threadIdx.x & 31;
     const u32 lane_bit = 1u << lane;
-    const int wib = threadIdx.x >> 5;
-    u64* ckey = s_key[wib];
-    u64* ccnt = s_cnt[wib];
-    unsigned char* owner = s_owner[wib];
-    for (int i = lane; i < kCacheSlots; i += 32) ckey[i] = kEmpty;
+    const u32 lt_mask = lane_bit - 1;
+    WarpSmem& w = s_warp[threadIdx.x >> 5];
+    for (int i = lane; i < kCacheSlots; i += 32) w.ckey[i] = kEmpty;
     __syncwarp();
 
     const Grid g = P.g;
+    const Table t = P.t;
     const u64 pol = evict_first_policy();
-    u32 pot = 0;      // warp-uniform: claimed keys + occupied cache entries
-    u32 claims = 0;   // per lane: keys this lane claimed in the table
-    u32 n_in = 0;     // per lane: in-bounds points
+    K1State st{0, 0, 0, 0};
     u64 n_valid = 0;  // warp-uniform: points examined
     bool stopped = false;
 
@@ -156,15 +243,15 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
                 return true;
             }
         }
-        u64 t = pending;
-        if (t == ~0ull) {
-            if (lane == 0) t = atomicAdd(&P.ctr->ticket, 1ull);
+        u64 tk = pending;
+        if (tk == ~0ull) {
+            if (lane == 0) tk = atomicAdd(&P.ctr->ticket, 1ull);
         }
-        t = __shfl_sync(kFull, t, 0);
+        tk = __shfl_sync(kFull, tk, 0);
         pending = ~0ull;
-        if (t >= P.n_seg) return false;
-        seg = t;
-        row0 = t * P.rows_per_seg;
+        if (tk >= P.n_seg) return false;
+        seg = tk;
+        row0 = tk * P.rows_per_seg;
         from_ticket = true;
         return true;
     };
@@ -184,97 +271,59 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         const u64 p_end = min(row_end * 32, P.n);
         if (lane == 0 && (from_ticket || P.n_partial_in == 0))
             pending = atomicAdd(&P.ctr->ticket, 1ull);
-        Rows cur, nxt;
+        Rows ra, rb;
         u64 p0 = row0 * 32;
         u32 left = (u32)min(p_end - p0, (u64)(32 * kBatch));
-        load_rows<kAligned>(P.xy, p0, left, lane, pol, cur);
+        load_rows<kAligned>(P.xy, p0, left, lane, pol, ra);
+        // Ping-pong between two register buffers (no copies): process one
+        // batch while the next one is in flight.
         while (true) {
-            const u64 pn = p0 + 32 * kBatch;
-            const u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
-            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, nxt);
+            u64 pn = p0 + 32 * kBatch;
+            u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
+            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, rb);
             n_valid += left;
-
-            u64 key[kBatch];
-            bool inb[kBatch];
-#pragma unroll
-            for (int b = 0; b < kBatch; ++b) {
-                inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
-                n_in += inb[b];
-                key[b] = inb[b] ? key_of<kNarrow>(g, cur.x[b], cur.y[b]) : kEmpty;
-            }
-            u32 peers[kBatch];
-#pragma unroll
-            for (int b = 0; b < kBatch; ++b) peers[b] = __match_any_sync(kFull, key[b]);
-
-            u32 pot_lane = 0;
-#pragma unroll
-            for (int b = 0; b < kBatch; ++b) {
-                const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
-                const u32 cs = cache_slot(key[b], g.bits_y);
-                // Hits: the slot already holds this key; distinct keys never
-                // hit the same slot, so leaders add without arbitration.
-                bool miss = false;
-                if (leader) {
-                    if (ckey[cs] == key[b])
-                        ccnt[cs] += __popc(peers[b]);
-                    else
-                        miss = true;
-                }
-                if (__any_sync(kFull, miss)) {
-                    // Misses: one leader per slot installs its key (flushing
-                    // the previous occupant to HBM); the rest go to HBM.
-                    if (miss) owner[cs] = (unsigned char)lane;
-                    __syncwarp();
-                    if (miss) {
-                        const u64 cnt = __popc(peers[b]);
-                        if (owner[cs] == lane) {
-                            const u64 ek = ckey[cs];
-                            if (ek != kEmpty) {
-                                const u32 c = table_add(P.t, ek, ccnt[cs]) ? 1u : 0u;
-                                claims += c;
-                                pot_lane += c;
-                            } else {
-                                pot_lane += 1;  // a new occupied cache entry
-                            }
-                            ckey[cs] = key[b];
-                            ccnt[cs] = cnt;
-                        } else {
-                            const u32 c = table_add(P.t, key[b], cnt) ? 1u : 0u;
-                            claims += c;
-                            pot_lane += c;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-            pot += __reduce_add_sync(kFull, pot_lane);
-            if (pot >= P.budget) {
-                // Out of budget: hand back the rest of this segment and the
-                // prefetched ticket.
+            process_batch<kNarrow>(g, t, ra, w, st, lane, lane_bit, lt_mask);
+            if (st.pot >= P.budget) {
                 if (left_n) record_partial(seg, pn / 32);
-                const u64 t = __shfl_sync(kFull, pending, 0);
-                if (t != ~0ull && t < P.n_seg) record_partial(t, t * P.rows_per_seg);
                 stopped = true;
                 break;
             }
             if (!left_n) break;
-            cur = nxt;
+            p0 = pn;
+            left = left_n;
+            pn = p0 + 32 * kBatch;
+            left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
+            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, ra);
+            n_valid += left;
+            process_batch<kNarrow>(g, t, rb, w, st, lane, lane_bit, lt_mask);
+            if (st.pot >= P.budget) {
+                if (left_n) record_partial(seg, pn / 32);
+                stopped = true;
+                break;
+            }
+            if (!left_n) break;
             p0 = pn;
             left = left_n;
         }
-        if (stopped) break;
+        if (stopped) {
+            // hand back the prefetched ticket too
+            const u64 tk = __shfl_sync(kFull, pending, 0);
+            if (tk != ~0ull && tk < P.n_seg) record_partial(tk, tk * P.rows_per_seg);
+            break;
+        }
         have = fetch(seg, row0, from_ticket);
     }
 
-    // Write back the cache.
+    // Write back staged entries and the cache.
+    flush_stage(t, w, st, lane);
     for (int i = lane; i < kCacheSlots; i += 32) {
-        const u64 k = ckey[i];
-        if (k != kEmpty) claims += table_add(P.t, k, ccnt[i]) ? 1u : 0u;
+        const u64 k = w.ckey[i];
+        if (k != kEmpty) st.claims += table_add(t, k, w.ccnt[i]) ? 1u : 0u;
     }
 
     // Counters: one atomic per warp.
-    const u32 wc = __reduce_add_sync(kFull, claims);
-    const u64 wi = __reduce_add_sync(kFull, n_in);
+    const u32 wc = __reduce_add_sync(kFull, st.claims);
+    const u64 wi = __reduce_add_sync(kFull, st.n_in);
     if (lane == 0) {
         if (wi) atomicAdd(&P.ctr->ingested, wi);
         if (n_valid > wi) atomicAdd(&P.ctr->skipped, n_valid - wi);
