@@ -70,31 +70,88 @@ struct Offsets {
     int n;
 };
 
-__global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bits_y,
-                        u32 bits_x, Offsets off, u32* parent) {
+__device__ __forceinline__ u32 lfind(volatile u32* lp, u32 x) {
+    u32 p;
+    while ((p = lp[x]) != x) x = p;
+    return x;
+}
+
+__device__ __forceinline__ void lunite(u32* lp, u32 a, u32 b) {
+    volatile u32* v = lp;
+    u32 ra = lfind(v, a), rb = lfind(v, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 tmp = ra;
+            ra = rb;
+            rb = tmp;
+        }
+        const u32 old = atomicCAS(lp + ra, ra, rb);
+        if (old == ra) return;
+        ra = lfind(v, old);
+        rb = lfind(v, rb);
+    }
+}
+
+constexpr int kStoredNb = 4;  // neighbour indices kept per tile for the warp-local pass
+
+// Union step. Tiles come in compaction (bucket) order, so a warp's 32
+// consecutive tiles are mostly spatial neighbours: edges between them are
+// resolved first in a shared-memory union-find over lanes (cheap, no global
+// contention), each local component is then linked to its smallest member
+// with one CAS, and only edges leaving the warp go through the global
+// union-find.
+__global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
+                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent) {
+    __shared__ u32 s_par[8][32];
     const u64 n_sig = *n_sig_p;
+    const int lane = threadIdx.x & 31;
+    u32* lp = s_par[threadIdx.x >> 5];
     const long long ymask = (1ll << bits_y) - 1;
     const long long xlim = 1ll << bits_x, ylim = 1ll << bits_y;
-    // Compaction emits tiles bucket by bucket, so consecutive indices are
-    // spatial neighbours of one cluster. Giving the 32 lanes of a warp tiles
-    // n/32 apart keeps their union CASes on different roots (no intra-warp
-    // contention); each lane's own neighbour probes still hit its bucket.
-    const u64 chunk = (n_sig + 31) / 32;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < 32 * chunk;
+    const u64 span = (n_sig + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
-        const u64 idx = (i & 31) * chunk + (i >> 5);
-        if (idx >= n_sig) continue;
-        const u64 key = sig_key[idx];
-        const long long kx = (long long)(key >> bits_y);
-        const long long ky = (long long)key & ymask;
-        for (int o = 0; o < off.n; ++o) {
-            const int2 d = off.d[o];
-            const long long nx = kx + d.x, ny = ky + d.y;
-            if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) continue;
-            const u64 nkey = ((u64)nx << bits_y) | (u64)ny;
-            const u64 v = table_find(t, nkey);
-            if (v != kEmpty && (v & kSigBit)) uf_unite(parent, (u32)idx, (u32)(v & ~kSigBit));
+        const u64 base = i - lane;
+        const bool valid = i < n_sig;
+        lp[lane] = lane;
+        u32 nb[kStoredNb];
+#pragma unroll
+        for (int o = 0; o < kStoredNb; ++o) nb[o] = 0xffffffffu;
+        if (valid) {
+            const u64 key = sig_key[i];
+            const long long kx = (long long)(key >> bits_y);
+            const long long ky = (long long)key & ymask;
+            for (int o = 0; o < off.n; ++o) {
+                const int2 d = off.d[o];
+                const long long nx = kx + d.x, ny = ky + d.y;
+                if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) continue;
+                const u64 v = table_find(t, ((u64)nx << bits_y) | (u64)ny);
+                if (v == kEmpty || !(v & kSigBit)) continue;
+                const u32 j = (u32)(v & ~kSigBit);
+                if (o < kStoredNb)
+                    nb[o] = j;
+                else
+                    uf_unite(parent, (u32)i, j);  // wide neighbourhoods (delta > 1)
+            }
         }
+        __syncwarp();
+        // warp-local edges
+#pragma unroll
+        for (int o = 0; o < kStoredNb; ++o)
+            if (nb[o] != 0xffffffffu && nb[o] >= base && nb[o] < base + 32)
+                lunite(lp, (u32)lane, nb[o] - (u32)base);
+        __syncwarp();
+        const u32 r = lfind(lp, (u32)lane);
+        if (valid && r != (u32)lane) {
+            const u32 target = (u32)base + r;  // < i: keeps parent[x] <= x
+            if (atomicCAS(parent + i, (u32)i, target) != (u32)i) uf_unite(parent, (u32)i, target);
+        }
+        // edges leaving the warp
+#pragma unroll
+        for (int o = 0; o < kStoredNb; ++o)
+            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + 32))
+                uf_unite(parent, (u32)i, nb[o]);
+        __syncwarp();
     }
 }
 
@@ -102,7 +159,8 @@ __global__ void k_union(const u64* sig_key, const u64* n_sig_p, Table t, u32 bit
 // concurrent walks never see (or leave behind) a non-root written late. (A
 // path-halving find here would race: another thread could overwrite
 // parent[i] with a non-root ancestor after i stored its root.)
-__global__ void k_compress(u32* parent, const u64* n_sig_p) {
+__global__ void k_compress(u32* parent, const u64* n_sig_p, u32* size, u64* npts, u64* min_key,
+                           int* root_cid) {
     const u64 n_sig = *n_sig_p;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
          i += (u64)gridDim.x * blockDim.x) {
@@ -110,6 +168,11 @@ __global__ void k_compress(u32* parent, const u64* n_sig_p) {
         u32 r = old, next;
         while (r > (next = ld_parent(parent + r))) r = next;
         if (r != old) parent[i] = r;
+        // initialise the per-root accumulators of k_root_reduce
+        size[i] = 0;
+        npts[i] = 0;
+        min_key[i] = kEmpty;
+        root_cid[i] = -1;
     }
 }
 
@@ -244,12 +307,8 @@ static int grid_for(u64 n, int n_sm, int per_sm = 8) {
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     const int gs = grid_for(A.n_sig, A.n_sm, 16);
     Offsets off{A.offsets, A.n_offsets};
-    cudaMemsetAsync(A.size, 0, A.n_sig * sizeof(u32), st);
-    cudaMemsetAsync(A.npts, 0, A.n_sig * sizeof(u64), st);
-    cudaMemsetAsync(A.min_key, 0xff, A.n_sig * sizeof(u64), st);
-    cudaMemsetAsync(A.root_cid, 0xff, A.n_sig * sizeof(int), st);
     k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent);
-    k_compress<<<gs, 256, 0, st>>>(A.parent, A.n_sig_dev);
+    k_compress<<<gs, 256, 0, st>>>(A.parent, A.n_sig_dev, A.size, A.npts, A.min_key, A.root_cid);
     k_root_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size, A.npts,
                                       A.min_key);
     k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,
