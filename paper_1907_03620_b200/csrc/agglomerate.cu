@@ -68,7 +68,17 @@ __device__ __forceinline__ void uf_unite(u32* parent, u32 a, u32 b) {
 struct Offsets {
     const int2* d;  // forward half of the delta-ball
     int n;
+    int cheb1;      // d == {(0,1), (1,-1), (1,0), (1,1)}: Chebyshev, delta 1
 };
+
+// Significant-tile index of (kx+dx, ky+dy), or 0xffffffff.
+__device__ __forceinline__ u32 sig_index(const Table& t, long long kx, long long ky, int dx, int dy,
+                                         u32 bits_y, long long xlim, long long ylim) {
+    const long long nx = kx + dx, ny = ky + dy;
+    if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) return 0xffffffffu;
+    const u64 v = table_find(t, ((u64)nx << bits_y) | (u64)ny);
+    return (v != kEmpty && (v & kSigBit)) ? (u32)(v & ~kSigBit) : 0xffffffffu;
+}
 
 __device__ __forceinline__ u32 lfind(volatile u32* lp, u32 x) {
     u32 p;
@@ -121,17 +131,28 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
             const u64 key = sig_key[i];
             const long long kx = (long long)(key >> bits_y);
             const long long ky = (long long)key & ymask;
-            for (int o = 0; o < off.n; ++o) {
-                const int2 d = off.d[o];
-                const long long nx = kx + d.x, ny = ky + d.y;
-                if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) continue;
-                const u64 v = table_find(t, ((u64)nx << bits_y) | (u64)ny);
-                if (v == kEmpty || !(v & kSigBit)) continue;
-                const u32 j = (u32)(v & ~kSigBit);
-                if (o < kStoredNb)
-                    nb[o] = j;
-                else
-                    uf_unite(parent, (u32)i, j);  // wide neighbourhoods (delta > 1)
+            if (off.cheb1) {
+                // Chebyshev delta 1: (x+1,y+1) touches (x,y+1) and (x+1,y), and
+                // (x+1,y-1) touches (x+1,y); when those are significant their
+                // own forward probes make the diagonal edge redundant, so the
+                // diagonals are probed only when needed (fewer unsuccessful
+                // probes, the long ones).
+                nb[0] = sig_index(t, kx, ky, 0, 1, bits_y, xlim, ylim);
+                nb[2] = sig_index(t, kx, ky, 1, 0, bits_y, xlim, ylim);
+                if (nb[2] == 0xffffffffu) {
+                    nb[1] = sig_index(t, kx, ky, 1, -1, bits_y, xlim, ylim);
+                    if (nb[0] == 0xffffffffu) nb[3] = sig_index(t, kx, ky, 1, 1, bits_y, xlim, ylim);
+                }
+            } else {
+                for (int o = 0; o < off.n; ++o) {
+                    const int2 d = off.d[o];
+                    const u32 j = sig_index(t, kx, ky, d.x, d.y, bits_y, xlim, ylim);
+                    if (j == 0xffffffffu) continue;
+                    if (o < kStoredNb)
+                        nb[o] = j;
+                    else
+                        uf_unite(parent, (u32)i, j);  // wide neighbourhoods (delta > 1)
+                }
             }
         }
         __syncwarp();
@@ -155,40 +176,31 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
     }
 }
 
-// Flatten: every thread writes only its own entry, and only with a root, so
-// concurrent walks never see (or leave behind) a non-root written late. (A
-// path-halving find here would race: another thread could overwrite
-// parent[i] with a non-root ancestor after i stored its root.)
-__global__ void k_compress(u32* parent, const u64* n_sig_p, u32* size, u64* npts, u64* min_key,
-                           int* root_cid) {
-    const u64 n_sig = *n_sig_p;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_sig;
-         i += (u64)gridDim.x * blockDim.x) {
-        const u32 old = ld_parent(parent + i);
-        u32 r = old, next;
-        while (r > (next = ld_parent(parent + r))) r = next;
-        if (r != old) parent[i] = r;
-        // initialise the per-root accumulators of k_root_reduce
-        size[i] = 0;
-        npts[i] = 0;
-        min_key[i] = kEmpty;
-        root_cid[i] = -1;
-    }
-}
-
-// Per-root reductions (size/points start at 0, min_key at kEmpty). Tiles of
-// one component sit in runs of consecutive indices (compaction order is
-// bucket order), so each warp first reduces its contiguous runs with a
-// segmented shuffle reduction and only run heads touch global memory.
-__global__ void k_root_reduce(const u32* parent, const u64* sig_key, const u64* sig_cnt,
-                              const u64* n_sig_p, u32* size, u64* npts, u64* min_key) {
+// Flatten + per-root reductions. Flatten: every thread writes only its own
+// entry, and only with a root, so concurrent walks never see (or leave
+// behind) a non-root written late (a path-halving find here would race:
+// another thread could overwrite parent[i] with a non-root ancestor after i
+// stored its root). Reductions: tile count, point count and smallest packed
+// key per root (accumulators were initialised by K2 / the load path). Tiles
+// of one component sit in runs of consecutive indices (compaction order is
+// bucket order), so each warp reduces its contiguous runs with a segmented
+// shuffle reduction and only run heads touch global memory.
+__global__ void k_compress_reduce(u32* parent, const u64* sig_key, const u64* sig_cnt,
+                                  const u64* n_sig_p, u32* size, u64* npts, u64* min_key) {
     const u64 n_sig = *n_sig_p;
     const int lane = threadIdx.x & 31;
     const u64 span = ((n_sig + 31) / 32) * 32;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
         const bool valid = i < n_sig;
-        const u32 r = valid ? parent[i] : 0xffffffffu;
+        u32 r = 0xffffffffu;
+        if (valid) {
+            const u32 old = ld_parent(parent + i);
+            u32 next;
+            r = old;
+            while (r > (next = ld_parent(parent + r))) r = next;
+            if (r != old) parent[i] = r;
+        }
         u32 cnt = valid ? 1u : 0u;
         u64 pts = valid && sig_cnt ? sig_cnt[i] : 0ull;
         u64 mk = valid ? sig_key[i] : kEmpty;
@@ -284,13 +296,18 @@ __global__ void k_label_tiles(const u32* parent, const int* root_cid, const u64*
 // every tile as significant with its dense index.
 __global__ void k_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
                              long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
-                             u64* sig_cnt, u32* parent) {
+                             u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                             int* root_cid) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x) {
         const u64 key = ((u64)(tx[i] - ox) << bits_y) | (u64)(ty[i] - oy);
         sig_key[i] = key;
         sig_cnt[i] = cnt ? cnt[i] : 0;
         parent[i] = (u32)i;
+        size[i] = 0;
+        npts[i] = 0;
+        min_key[i] = kEmpty;
+        root_cid[i] = -1;
         const u64 slot = table_claim(t, key);
         t.slots[slot].count = kSigBit | i;
     }
@@ -306,11 +323,10 @@ static int grid_for(u64 n, int n_sm, int per_sm = 8) {
 
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     const int gs = grid_for(A.n_sig, A.n_sm, 16);
-    Offsets off{A.offsets, A.n_offsets};
+    Offsets off{A.offsets, A.n_offsets, A.cheb1};
     k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent);
-    k_compress<<<gs, 256, 0, st>>>(A.parent, A.n_sig_dev, A.size, A.npts, A.min_key, A.root_cid);
-    k_root_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size, A.npts,
-                                      A.min_key);
+    k_compress_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size,
+                                          A.npts, A.min_key);
     k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,
                                        A.root_key, A.root_idx, A.ctr);
     return cudaGetLastError();
@@ -347,9 +363,11 @@ cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_ou
 
 cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
                               long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
-                              u64* sig_cnt, u32* parent, int n_sm, cudaStream_t st) {
+                              u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                              int* root_cid, int n_sm, cudaStream_t st) {
     k_load_tiles<<<grid_for(n, n_sm), 256, 0, st>>>(tx, ty, cnt, n, ox, oy, bits_y, t, sig_key,
-                                                     sig_cnt, parent);
+                                                     sig_cnt, parent, size, npts, min_key,
+                                                     root_cid);
     return cudaGetLastError();
 }
 

@@ -661,7 +661,8 @@ rg_status prune_impl(rg_ctx* ctx) {
     zero_field(ctx, &ctx->ctr->n_sig);
     if (ctx->slots && ctx->used) {
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
-                          ctx->parent, ctx->ctr, ctx->n_sm, ctx->st));
+                          ctx->parent, ctx->size, ctx->npts, ctx->min_key, ctx->root_cid, ctx->ctr,
+                          ctx->n_sm, ctx->st));
         ++ctx->launches;
     }
     CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, sizeof(u64), cudaMemcpyDeviceToHost,
@@ -686,6 +687,14 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
         ctx->state = rg_ctx::kAgg;
         return RG_OK;
     }
+    if (ctx->state == rg_ctx::kAgg) {
+        // agglomerating the same set again: K2 / the load path initialised
+        // the per-root accumulators only once
+        CK(cudaMemsetAsync(ctx->size, 0, ctx->n_sig * sizeof(u32), ctx->st));
+        CK(cudaMemsetAsync(ctx->npts, 0, ctx->n_sig * sizeof(u64), ctx->st));
+        CK(cudaMemsetAsync(ctx->min_key, 0xff, ctx->n_sig * sizeof(u64), ctx->st));
+        CK(cudaMemsetAsync(ctx->root_cid, 0xff, ctx->n_sig * sizeof(int), ctx->st));
+    }
     AggLaunch A;
     A.sig_key = ctx->sig_key;
     A.sig_cnt = ctx->sig_cnt;
@@ -696,6 +705,7 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
     A.bits_x = ctx->res.bits_x;
     A.offsets = ctx->offsets;
     A.n_offsets = ctx->n_offsets;
+    A.cheb1 = ctx->p.metric == RG_METRIC_CHEBYSHEV && ctx->p.distance == 1;
     A.mu = ctx->p.min_cluster_size;
     A.parent = ctx->parent;
     A.size = ctx->size;
@@ -712,7 +722,7 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);
     CK(launch_agglomerate(A, ctx->st));
-    ctx->launches += 4;
+    ctx->launches += 3;
     CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
                        cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -1160,8 +1170,8 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
         CK(cudaMemcpyAsync(dty, ty, n * 8, mk, ctx->st));
         if (count) CK(cudaMemcpyAsync(dcnt, count, n * 8, mk, ctx->st));
         CK(launch_load_tiles(dtx, dty, dcnt, n, res.origin_x, res.origin_y, res.bits_y,
-                             table_of(ctx), ctx->sig_key, ctx->sig_cnt, ctx->parent, ctx->n_sm,
-                             ctx->st));
+                             table_of(ctx), ctx->sig_key, ctx->sig_cnt, ctx->parent, ctx->size,
+                             ctx->npts, ctx->min_key, ctx->root_cid, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
         dfree(dtx);

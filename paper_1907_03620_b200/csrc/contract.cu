@@ -373,17 +373,57 @@ __global__ void k_first_oob(const double* xy, u64 n, Grid g, u64* first) {
 // K2: TileAccumulator::prune accumulator.hpp:160-174 — keep count >= tau.
 // Each significant slot gets a dense index, its key/count are written to the
 // compact arrays, the slot's value word becomes SIG_BIT | index and the
-// union-find parent is initialised. A warp owns 32 x kK2Items consecutive
-// slots (coalesced 16-byte loads, all issued before any use) and reserves its
-// output range with one atomic; no block-wide barrier sits on the path, so
-// the atomic's round trip overlaps other warps' loads.
+// union-find parent is initialised. A warp streams 32 x kK2Items consecutive
+// slots per step (coalesced 16-byte loads, all in flight together) and only
+// stages the slot numbers of significant entries in shared memory; every
+// >= 256 staged entries it reserves output space with one atomic and writes
+// them out contiguously (the slots are re-read from L1/L2). Waiting on the
+// reservation is paid once per 256 outputs instead of once per step.
 constexpr int kK2Items = 8;
-__global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, u64* sig_key,
-                                                 u64* sig_cnt, u32* parent, Counters* ctr) {
+constexpr int kK2Stage = 256 + 32 * kK2Items;
+
+struct K2Out {
+    u64* sig_key;
+    u64* sig_cnt;
+    u32* parent;
+    // per-root accumulators of agglomeration, initialised here
+    u32* size;
+    u64* npts;
+    u64* min_key;
+    int* root_cid;
+};
+
+__device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n, const K2Out& o,
+                                         Counters* ctr, int lane) {
+    u64 at = 0;
+    if (lane == 0) at = atomicAdd(&ctr->n_sig, (u64)n);
+    at = __shfl_sync(kFull, at, 0);
+    for (u32 e = lane; e < n; e += 32) {
+        const u32 i = s_idx[e];
+        u64 k, v;
+        ld_slot(t.slots + i, k, v);
+        const u64 pos = at + e;
+        o.sig_key[pos] = k;
+        o.sig_cnt[pos] = v;
+        o.parent[pos] = (u32)pos;
+        o.size[pos] = 0;
+        o.npts[pos] = 0;
+        o.min_key[pos] = kEmpty;
+        o.root_cid[pos] = -1;
+        t.slots[i].count = kSigBit | pos;
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, K2Out out,
+                                                 Counters* ctr) {
+    __shared__ u32 s_stage[8][kK2Stage];
     const int lane = threadIdx.x & 31;
+    u32* s_idx = s_stage[threadIdx.x >> 5];
     const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
     const u64 n_warps = ((u64)gridDim.x * blockDim.x) >> 5;
     constexpr u64 per_warp = 32ull * kK2Items;
+    u32 slen = 0;  // warp-uniform
     for (u64 base = warp * per_warp; base < cap; base += n_warps * per_warp) {
         u64 k[kK2Items], v[kK2Items];
 #pragma unroll
@@ -406,22 +446,18 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, u64*
             if (lane >= o) incl += y;
         }
         const u32 total = __shfl_sync(kFull, incl, 31);
-        if (total == 0) continue;
-        u64 at = 0;
-        if (lane == 31) at = atomicAdd(&ctr->n_sig, (u64)total);
-        u64 pos = __shfl_sync(kFull, at, 31) + incl - nsig;
+        u32 p = slen + incl - nsig;
 #pragma unroll
-        for (int j = 0; j < kK2Items; ++j) {
-            if (k[j] != kEmpty && v[j] >= tau) {
-                const u64 i = base + j * 32 + lane;
-                sig_key[pos] = k[j];
-                sig_cnt[pos] = v[j];
-                parent[pos] = (u32)pos;
-                t.slots[i].count = kSigBit | pos;
-                ++pos;
-            }
+        for (int j = 0; j < kK2Items; ++j)
+            if (k[j] != kEmpty && v[j] >= tau) s_idx[p++] = (u32)(base + j * 32 + lane);
+        slen += total;
+        __syncwarp();
+        if (slen >= 256) {
+            k2_flush(t, s_idx, slen, out, ctr, lane);
+            slen = 0;
         }
     }
+    if (slen) k2_flush(t, s_idx, slen, out, ctr, lane);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -498,11 +534,13 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 }
 
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           Counters* ctr, int n_sm, cudaStream_t st) {
+                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
+                           int n_sm, cudaStream_t st) {
     const u64 per_block = 256ull * kK2Items;
     const u64 want = (cap + per_block - 1) / per_block;
     const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
-    k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, sig_key, sig_cnt, parent, ctr);
+    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid};
+    k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, o, ctr);
     return cudaGetLastError();
 }
 

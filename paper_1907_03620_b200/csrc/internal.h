@@ -31,7 +31,8 @@ cudaError_t launch_table_fold(const Slot* src, u64 n_src, Table dst, u64* claime
 cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           Counters* ctr, int n_sm, cudaStream_t st);
+                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
+                           int n_sm, cudaStream_t st);
 
 struct AggLaunch {
     const u64* sig_key;
@@ -42,6 +43,7 @@ struct AggLaunch {
     u32 bits_y, bits_x;
     const int2* offsets;
     int n_offsets;
+    int cheb1;  // offsets are exactly Chebyshev delta 1
     u64 mu;
     u32* parent;
     u32* size;
@@ -66,7 +68,8 @@ cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_ou
                        const u32* v_in, u32* v_out, u64 n, int bits, cudaStream_t st);
 cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
                               long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
-                              u64* sig_cnt, u32* parent, int n_sm, cudaStream_t st);
+                              u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                              int* root_cid, int n_sm, cudaStream_t st);
 
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
                                 int* labels, int n_sm, cudaStream_t st);
