@@ -1382,8 +1382,8 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         return RG_OK;
     }
     if (kind == RG_MEM_DEVICE) {
-        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, labels, ctx->n_sm,
-                               ctx->st));
+        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, labels, ctx->narrow,
+                               ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
         return RG_OK;
@@ -1397,7 +1397,7 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         CK(cudaMemcpyAsync(ctx->stage[b], xy + 2 * off, len * 16, cudaMemcpyHostToDevice,
                            ctx->st));
         CK(launch_label_points(ctx->stage[b], len, ctx->grid, table_of(ctx), ctx->tile_cid,
-                               ctx->lstage[b], ctx->n_sm, ctx->st));
+                               ctx->lstage[b], ctx->narrow, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaMemcpyAsync(labels + off, ctx->lstage[b], len * 4, cudaMemcpyDeviceToHost,
                            ctx->st));

@@ -98,12 +98,24 @@ struct Rows {
 template <bool kAligned>
 __device__ __forceinline__ void load_rows(const double* xy, u64 p0, u32 left, int lane, u64 pol,
                                           Rows& o) {
-    const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
+    if (kAligned && left == 32 * kBatch) {
+        // Full batch (all but a segment's last batch): one base pointer,
+        // immediate offsets, no per-row predicates.
+        const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const double2 v = ld_point_stream(base + b * 32, pol);
+            o.x[b] = v.x;
+            o.y[b] = v.y;
+        }
+        return;
+    }
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
         if ((u32)(b * 32 + lane) < left) {
             if (kAligned) {
-                const double2 v = ld_point_stream(base + b * 32, pol);
+                const double2 v =
+                    ld_point_stream(reinterpret_cast<const double2*>(xy) + p0 + b * 32 + lane, pol);
                 o.x[b] = v.x;
                 o.y[b] = v.y;
             } else {
@@ -157,7 +169,10 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
     for (int b = 0; b < kBatch; ++b) {
         inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
         s.n_in += inb[b];
-        key[b] = inb[b] ? key_of<kNarrow>(g, cur.x[b], cur.y[b]) : kEmpty;
+        // Computed unconditionally (no branch): for out-of-bounds or NaN
+        // lanes the conversion result is meaningless and replaced by EMPTY.
+        const u64 k = key_of<kNarrow>(g, cur.x[b], cur.y[b]);
+        key[b] = inb[b] ? k : kEmpty;
     }
     u32 peers[kBatch];
 #pragma unroll

@@ -72,7 +72,7 @@ cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u6
                               int* root_cid, int n_sm, cudaStream_t st);
 
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
-                                int* labels, int n_sm, cudaStream_t st);
+                                int* labels, bool narrow, int n_sm, cudaStream_t st);
 
 // small utility kernels (api.cu)
 cudaError_t launch_iota(u32* out, u64 n, int n_sm, cudaStream_t st);
