@@ -109,6 +109,16 @@ class ClockSampler:
                 "samples": len(self.sm), "source": "NVML, 2 ms period, timed region only"}
 
 
+def k1_traffic(n: int):
+    """dram bytes per K1 launch from the committed ncu --set full capture
+    (profiles/r01/k1_traffic.json), scaled to this workload; None if absent."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r01" / "k1_traffic.json").read_text())
+        return d["traffic_bytes_per_launch"] * n / (d["algorithmic_bytes_per_launch"] / BYTES_PER_POINT)
+    except Exception:
+        return None
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
@@ -306,7 +316,8 @@ def ours(args) -> None:
                    else "inputs smaller than L2: not flushed",
                    "parallelism": "1 GPU" if world == 1 else f"{world} ranks, independent shards (no cross-rank merge)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": k1_traffic(n) if cfg == 4 else None,
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01)",
                      "kernel": "K1 contraction (k_contract), 16 B/point, ms from CUDA events on the launch stream",
                      "peak_source": peak_src,
                      "end_to_end_frac": (BYTES_PER_POINT * n / (ms_step / 1e3) / 1e9) / peak},
