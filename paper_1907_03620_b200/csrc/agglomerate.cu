@@ -104,26 +104,37 @@ __device__ __forceinline__ void lunite(u32* lp, u32 a, u32 b) {
 
 constexpr int kStoredNb = 4;  // neighbour indices kept per tile for the warp-local pass
 
-// Union step. Tiles come in compaction (bucket) order, so a warp's 32
+// Union step. Tiles come in compaction (bucket) order, so a block's 256
 // consecutive tiles are mostly spatial neighbours: edges between them are
-// resolved first in a shared-memory union-find over lanes (cheap, no global
-// contention), each local component is then linked to its smallest member
-// with one CAS, and only edges leaving the warp go through the global
-// union-find.
+// resolved first in a shared-memory union-find (cheap, no global contention),
+// each local component is then linked to its smallest member with one CAS,
+// and only edges leaving the window go through the global union-find.
+#ifndef RG_UNION_WINDOW
+#define RG_UNION_WINDOW 256
+#endif
+constexpr int kUnionWindow = RG_UNION_WINDOW;  // = blockDim.x
+
+__device__ __forceinline__ void window_sync() {
+    if (kUnionWindow == 32)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
                                                u32 bits_y, u32 bits_x, Offsets off, u32* parent) {
-    __shared__ u32 s_par[8][32];
+    __shared__ u32 s_par[256];
     const u64 n_sig = *n_sig_p;
-    const int lane = threadIdx.x & 31;
-    u32* lp = s_par[threadIdx.x >> 5];
+    const u32 loc = threadIdx.x % kUnionWindow;
+    u32* lp = s_par + (threadIdx.x - loc);
     const long long ymask = (1ll << bits_y) - 1;
     const long long xlim = 1ll << bits_x, ylim = 1ll << bits_y;
-    const u64 span = (n_sig + 31) / 32 * 32;
+    const u64 span = (n_sig + 255) / 256 * 256;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
-        const u64 base = i - lane;
+        const u64 base = i - loc;
         const bool valid = i < n_sig;
-        lp[lane] = lane;
+        lp[loc] = loc;
         u32 nb[kStoredNb];
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o) nb[o] = 0xffffffffu;
@@ -155,24 +166,24 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
                 }
             }
         }
-        __syncwarp();
-        // warp-local edges
+        window_sync();
+        // window-local edges
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (nb[o] != 0xffffffffu && nb[o] >= base && nb[o] < base + 32)
-                lunite(lp, (u32)lane, nb[o] - (u32)base);
-        __syncwarp();
-        const u32 r = lfind(lp, (u32)lane);
-        if (valid && r != (u32)lane) {
+            if (nb[o] != 0xffffffffu && nb[o] >= base && nb[o] < base + kUnionWindow)
+                lunite(lp, loc, nb[o] - (u32)base);
+        window_sync();
+        const u32 r = lfind(lp, loc);
+        if (valid && r != loc) {
             const u32 target = (u32)base + r;  // < i: keeps parent[x] <= x
             if (atomicCAS(parent + i, (u32)i, target) != (u32)i) uf_unite(parent, (u32)i, target);
         }
-        // edges leaving the warp
+        // edges leaving the window
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + 32))
+            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + kUnionWindow))
                 uf_unite(parent, (u32)i, nb[o]);
-        __syncwarp();
+        window_sync();
     }
 }
 
