@@ -11,16 +11,17 @@
 // round-to-nearest multiplication guarantees every in-bounds point lands in
 // [origin, origin + 2^bits).
 //
-// Hash table. One open-addressed table of 16-byte slots {u64 key, u64 count}
-// in HBM replaces TileCounts (accumulator.hpp:23-99). It is bucketed for
-// spatial locality: the grid is cut into 4x4-tile blocks, a block hashes to a
-// bucket of 16 slots (256 B, two cache lines) and a tile always sits at the
-// slot of its position inside the block. Collisions probe linearly bucket by
-// bucket at the same position, so the table is 16 interleaved linear-probing
-// tables. A cluster's tiles therefore share one or a few buckets: contraction
-// updates, neighbour probes during agglomeration and per-point lookups touch
-// a handful of lines instead of one random line per tile, and compaction
-// (which scans slot order) emits spatially adjacent tiles next to each other.
+// Hash table. One open-addressed, linear-probing table of 16-byte slots
+// {u64 key, u64 count} in HBM replaces TileCounts (accumulator.hpp:23-99).
+// Its hash keeps spatial locality: the grid is cut into 4x4-tile blocks, a
+// block hashes to a bucket of 16 slots (256 B, two cache lines) and a tile's
+// home slot is its position inside the block; collisions probe slot by slot
+// from there (plain linear probing, so every slot is reachable and the
+// global load bound is the only fill limit). A cluster's tiles therefore
+// share one or a few buckets: contraction updates, neighbour probes during
+// agglomeration and per-point lookups touch a handful of lines instead of one
+// random line per tile, and compaction (which scans slot order) emits
+// spatially adjacent tiles next to each other.
 // Keys are claimed with a 64-bit CAS and never change afterwards, so probes
 // may use plain (L1-cacheable) loads; counts are bumped with RED.ADD.64.
 // After pruning, the count word of a significant slot is overwritten with
@@ -62,7 +63,7 @@ constexpr u32 kBucketSlots = 1u << (2 * kBlockBits);  // 16 slots per bucket
 
 struct Table {
     Slot* slots;
-    u64 bmask;     // buckets - 1 (bucket count is a power of two)
+    u64 smask;     // slots - 1 (slot count is a power of two)
     u32 shift;     // 64 - log2(buckets)
     u32 bits_y;    // key packing of the keys stored in this table (>= kBlockBits)
 };
@@ -129,10 +130,9 @@ __device__ __forceinline__ double2 ld_point_stream(const double2* p, u64 pol) {
 // Insert-or-add into the HBM table. Returns true when this call claimed a new
 // slot (a new distinct tile). TileCounts::add accumulator.hpp:33-50.
 __device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
-    u64 b = home_bucket(key, t);
-    const u32 pos = in_bucket(key, t);
+    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
     while (true) {
-        Slot* s = t.slots + ((b << (2 * kBlockBits)) | pos);
+        Slot* s = t.slots + i;
         u64 k = ld_key(s);
         if (k == key) {
             red_add(&s->count, cnt);
@@ -149,34 +149,31 @@ __device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
                 return false;
             }
         }
-        b = (b + 1) & t.bmask;
+        i = (i + 1) & t.smask;
     }
 }
 
 // Lookup: returns the slot's value word, or kEmpty when the key is absent.
 // TileCounts::count_of accumulator.hpp:53-61.
 __device__ __forceinline__ u64 table_find(const Table& t, u64 key) {
-    u64 b = home_bucket(key, t);
-    const u32 pos = in_bucket(key, t);
+    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
     while (true) {
         u64 k, v;
-        ld_slot(t.slots + ((b << (2 * kBlockBits)) | pos), k, v);
+        ld_slot(t.slots + i, k, v);
         if (k == key) return v;
         if (k == kEmpty) return kEmpty;
-        b = (b + 1) & t.bmask;
+        i = (i + 1) & t.smask;
     }
 }
 
 // Claim a slot for a key known to be absent (rehash / load paths); returns
 // the slot index.
 __device__ __forceinline__ u64 table_claim(const Table& t, u64 key) {
-    u64 b = home_bucket(key, t);
-    const u32 pos = in_bucket(key, t);
+    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
     while (true) {
-        const u64 i = (b << (2 * kBlockBits)) | pos;
         const u64 old = atomicCAS(&t.slots[i].key, kEmpty, key);
         if (old == kEmpty || old == key) return i;
-        b = (b + 1) & t.bmask;
+        i = (i + 1) & t.smask;
     }
 }
 

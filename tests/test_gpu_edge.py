@@ -232,3 +232,16 @@ def test_hot_spot_single_tile():
     flat = pl.flat()
     assert flat.tx.tolist() == [123] and flat.count.tolist() == [n]
     assert st.n_clusters == 0  # one tile < mu
+
+
+def test_lattice_same_block_position():
+    """Every tile at the same position inside its 4x4 (and 8x8) table block:
+    a probe scheme that stayed at the home position would overflow."""
+    gp = GridParams(precision=3.0, threshold=1, min_cluster_size=1)
+    i, j = np.meshgrid(np.arange(400), np.arange(400), indexing="ij")
+    tx, ty = (8 * i).ravel(), (8 * j).ravel()
+    pts = np.stack([(tx + 0.5) / 1000.0, (ty + 0.5) / 1000.0], 1)
+    gp.capacity_hint = 1
+    flat = cluster_flat(pts, gp)
+    assert_same(flat, oracle(pts, gp))
+    assert flat.n_clusters == 160_000
