@@ -304,7 +304,7 @@ Grid make_grid(const rg_params& p) {
 Table make_table(Slot* slots, u64 cap, u32 bits_y) {
     Table t;
     t.slots = slots;
-    t.smask = cap - 1;
+    t.bmask = cap / kBucketSlots - 1;
     t.shift = 64 - log2u(cap / kBucketSlots);
     t.bits_y = bits_y;
     return t;

@@ -11,16 +11,18 @@
 // round-to-nearest multiplication guarantees every in-bounds point lands in
 // [origin, origin + 2^bits).
 //
-// Hash table. One open-addressed, linear-probing table of 16-byte slots
-// {u64 key, u64 count} in HBM replaces TileCounts (accumulator.hpp:23-99).
-// Its hash keeps spatial locality: the grid is cut into 4x4-tile blocks, a
-// block hashes to a bucket of 16 slots (256 B, two cache lines) and a tile's
-// home slot is its position inside the block; collisions probe slot by slot
-// from there (plain linear probing, so every slot is reachable and the
-// global load bound is the only fill limit). A cluster's tiles therefore
-// share one or a few buckets: contraction updates, neighbour probes during
-// agglomeration and per-point lookups touch a handful of lines instead of one
-// random line per tile, and compaction (which scans slot order) emits
+// Hash table. One open-addressed table of 16-byte slots {u64 key, u64 count}
+// in HBM replaces TileCounts (accumulator.hpp:23-99). It is bucketed for
+// spatial locality: the grid is cut into 4x4-tile blocks, a block hashes to a
+// bucket of 16 slots (256 B, two cache lines) and a tile's slot inside the
+// bucket is its in-block position XOR a per-block hash nibble (so inputs
+// whose tiles share an in-block position, e.g. lattices, still spread over
+// all 16 slots). Collisions probe bucket by bucket at the same in-bucket
+// slot; after a full cycle of buckets the slot advances, so every slot is
+// reachable and the global load bound is the only fill limit. A cluster's
+// tiles share one or a few buckets: contraction updates, neighbour probes
+// during agglomeration and per-point lookups touch a handful of lines instead
+// of one random line per tile, and compaction (which scans slot order) emits
 // spatially adjacent tiles next to each other.
 // Keys are claimed with a 64-bit CAS and never change afterwards, so probes
 // may use plain (L1-cacheable) loads; counts are bumped with RED.ADD.64.
@@ -63,24 +65,34 @@ constexpr u32 kBucketSlots = 1u << (2 * kBlockBits);  // 16 slots per bucket
 
 struct Table {
     Slot* slots;
-    u64 smask;     // slots - 1 (slot count is a power of two)
+    u64 bmask;     // buckets - 1 (bucket count is a power of two)
     u32 shift;     // 64 - log2(buckets)
     u32 bits_y;    // key packing of the keys stored in this table (>= kBlockBits)
 };
 
-// First slot probed for a key and the in-bucket position it keeps on every
-// probe. Fibonacci hashing of the block coordinate; the reference's TileHash
-// (core.hpp:56-68) only affects probe order, never results.
-__device__ __forceinline__ u64 home_bucket(u64 key, const Table& t) {
-    const u64 ky = key & ((1ull << t.bits_y) - 1);
-    const u64 block = ((key >> (t.bits_y + kBlockBits)) << (t.bits_y - kBlockBits)) | (ky >> kBlockBits);
-    return (block * 0x9E3779B97F4A7C15ull) >> t.shift;
-}
-__device__ __forceinline__ u32 in_bucket(u64 key, const Table& t) {
-    const u32 kx = (u32)(key >> t.bits_y) & ((1u << kBlockBits) - 1);
-    const u32 ky = (u32)key & ((1u << kBlockBits) - 1);
-    return (kx << kBlockBits) | ky;
-}
+// Probe sequence of a key: Fibonacci hashing of the block coordinate picks
+// the home bucket and (next bits) the nibble that scrambles the in-bucket
+// slot. The reference's TileHash (core.hpp:56-68) only affects probe order,
+// never results.
+struct Probe {
+    u64 b0, b;
+    u32 pos;
+    __device__ __forceinline__ Probe(u64 key, const Table& t) {
+        const u64 ky = key & ((1ull << t.bits_y) - 1);
+        const u64 block =
+            ((key >> (t.bits_y + kBlockBits)) << (t.bits_y - kBlockBits)) | (ky >> kBlockBits);
+        const u64 h = block * 0x9E3779B97F4A7C15ull;
+        b0 = b = h >> t.shift;
+        const u32 kx = (u32)(key >> t.bits_y) & ((1u << kBlockBits) - 1);
+        const u32 kyl = (u32)key & ((1u << kBlockBits) - 1);
+        pos = ((kx << kBlockBits) | kyl) ^ ((u32)(h >> (t.shift - 2 * kBlockBits)) & (kBucketSlots - 1));
+    }
+    __device__ __forceinline__ u64 slot() const { return (b << (2 * kBlockBits)) | pos; }
+    __device__ __forceinline__ void next(const Table& t) {
+        b = (b + 1) & t.bmask;
+        if (b == b0) pos = (pos + 1) & (kBucketSlots - 1);
+    }
+};
 
 // Bounds::contains core.hpp:33-35 — closed interval; NaN compares false.
 __device__ __forceinline__ bool in_bounds(const Grid& g, double x, double y) {
@@ -130,9 +142,9 @@ __device__ __forceinline__ double2 ld_point_stream(const double2* p, u64 pol) {
 // Insert-or-add into the HBM table. Returns true when this call claimed a new
 // slot (a new distinct tile). TileCounts::add accumulator.hpp:33-50.
 __device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
-    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
+    Probe p(key, t);
     while (true) {
-        Slot* s = t.slots + i;
+        Slot* s = t.slots + p.slot();
         u64 k = ld_key(s);
         if (k == key) {
             red_add(&s->count, cnt);
@@ -149,31 +161,32 @@ __device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
                 return false;
             }
         }
-        i = (i + 1) & t.smask;
+        p.next(t);
     }
 }
 
 // Lookup: returns the slot's value word, or kEmpty when the key is absent.
 // TileCounts::count_of accumulator.hpp:53-61.
 __device__ __forceinline__ u64 table_find(const Table& t, u64 key) {
-    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
+    Probe p(key, t);
     while (true) {
         u64 k, v;
-        ld_slot(t.slots + i, k, v);
+        ld_slot(t.slots + p.slot(), k, v);
         if (k == key) return v;
         if (k == kEmpty) return kEmpty;
-        i = (i + 1) & t.smask;
+        p.next(t);
     }
 }
 
 // Claim a slot for a key known to be absent (rehash / load paths); returns
 // the slot index.
 __device__ __forceinline__ u64 table_claim(const Table& t, u64 key) {
-    u64 i = (home_bucket(key, t) << (2 * kBlockBits)) | in_bucket(key, t);
+    Probe p(key, t);
     while (true) {
+        const u64 i = p.slot();
         const u64 old = atomicCAS(&t.slots[i].key, kEmpty, key);
         if (old == kEmpty || old == key) return i;
-        i = (i + 1) & t.smask;
+        p.next(t);
     }
 }
 
