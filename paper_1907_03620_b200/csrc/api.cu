@@ -406,9 +406,10 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
     const u64 w0 = (u64)ctx->max_warps;
     const u64 batch = (u64)contract_batch_rows();
     u64 rps = rows / (8 * w0);
-    rps = std::max<u64>(batch, std::min<u64>(64, rps)) / batch * batch;
+    rps = std::max<u64>(batch, std::min<u64>(256, rps)) / batch * batch;
     const u64 n_seg = (rows + rps - 1) / rps;
-    const u64 W = (std::min(w0, n_seg) + 7) / 8 * 8;  // whole blocks of 8 warps (w0 is a multiple of 8)
+    const u64 bw = (u64)contract_block_warps();
+    const u64 W = (std::min(w0, n_seg) + bw - 1) / bw * bw;  // whole blocks (w0 is a multiple)
     // A warp checks its budget once per batch of rows, so it can overshoot
     // by batch*32 - 1 keys: the table must hold soft + W*batch*32 keys, i.e.
     // (1 - kMaxLoad) * cap > W * batch * 32.

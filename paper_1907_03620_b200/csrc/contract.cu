@@ -32,14 +32,17 @@
 
 namespace rg {
 
-constexpr int kWarpsPerBlock = 8;
+#ifndef RG_K1_WARPS
+#define RG_K1_WARPS 4
+#endif
+constexpr int kWarpsPerBlock = RG_K1_WARPS;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kCacheSlots = 128;
 #ifndef RG_K1_BATCH
 #define RG_K1_BATCH 2
 #endif
 #ifndef RG_K1_MINBLOCKS
-#define RG_K1_MINBLOCKS 4
+#define RG_K1_MINBLOCKS 8
 #endif
 constexpr int kBatch = RG_K1_BATCH;  // rows per batch; the next batch is prefetched while one is processed
 
@@ -224,20 +227,42 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
     }
 }
 
+// Asynchronous 16-byte global->shared copy (LDGSTS), L1-bypassing, with an
+// L2 evict-first policy: the points are read exactly once.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, u64 pol) {
+    const u32 s = (u32)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+#ifndef RG_K1_RING
+#define RG_K1_RING 8
+#endif
+constexpr int kRing = RG_K1_RING;  // rows in flight per warp (multiple of kBatch)
+
 template <bool kAligned, bool kNarrow>
 __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ WarpSmem s_warp[kWarpsPerBlock];
+    __shared__ __align__(16) double2 s_ring[kWarpsPerBlock][kRing][32];
 
     const int lane = threadIdx.x & 31;
     const u32 lane_bit = 1u << lane;
     const u32 lt_mask = lane_bit - 1;
     WarpSmem& w = s_warp[threadIdx.x >> 5];
+    double2 (*ring)[32] = s_ring[threadIdx.x >> 5];
     for (int i = lane; i < kCacheSlots; i += 32) w.ckey[i] = kEmpty;
     __syncwarp();
 
     const Grid g = P.g;
     const Table t = P.t;
     const u64 pol = evict_first_policy();
+    const double2* pts = reinterpret_cast<const double2*>(P.xy);
     K1State st{0, 0, 0, 0};
     u64 n_valid = 0;  // warp-uniform: points examined
     bool stopped = false;
@@ -277,48 +302,59 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
             P.partial_out[at].next_row = row;
         }
     };
+    // Issue the copy of row `row` (if it exists) into its ring slot; one
+    // commit group per row on every lane keeps the group count uniform.
+    auto issue = [&](u64 row, u64 row_end, u64 row0) {
+        const u64 idx = row * 32 + lane;
+        if (row < row_end && idx < P.n) {
+            double2* dst = &ring[(row - row0) % kRing][lane];
+            if (kAligned) {
+                cp_async16(dst, pts + idx, pol);
+            } else {
+                dst->x = P.xy[2 * idx];
+                dst->y = P.xy[2 * idx + 1];
+            }
+        }
+        cp_async_commit();
+    };
 
     u64 seg, row0;
     bool from_ticket;
     bool have = fetch(seg, row0, from_ticket);
     while (have) {
         const u64 row_end = min((seg + 1) * P.rows_per_seg, P.n_rows);
-        const u64 p_end = min(row_end * 32, P.n);
         if (lane == 0 && (from_ticket || P.n_partial_in == 0))
             pending = atomicAdd(&P.ctr->ticket, 1ull);
-        Rows ra, rb;
-        u64 p0 = row0 * 32;
-        u32 left = (u32)min(p_end - p0, (u64)(32 * kBatch));
-        load_rows<kAligned>(P.xy, p0, left, lane, pol, ra);
-        // Ping-pong between two register buffers (no copies): process one
-        // batch while the next one is in flight.
-        while (true) {
-            u64 pn = p0 + 32 * kBatch;
-            u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
-            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, rb);
+#pragma unroll
+        for (int k = 0; k < kRing; ++k) issue(row0 + k, row_end, row0);
+        for (u64 r = row0; r < row_end; r += kBatch) {
+            // rows r .. r+kBatch-1 have landed once at most kRing-kBatch
+            // younger groups are pending
+            cp_async_wait<kRing - kBatch>();
+            Rows cur;
+            u32 left = 0;
+#pragma unroll
+            for (int b = 0; b < kBatch; ++b) {
+                const u64 row = r + b;
+                const u64 idx = row * 32 + lane;
+                if (row < row_end && idx < P.n) {
+                    const double2 v = ring[(row - row0) % kRing][lane];
+                    cur.x[b] = v.x;
+                    cur.y[b] = v.y;
+                } else {
+                    cur.x[b] = cur.y[b] = __longlong_as_double(0x7ff8000000000000ll);
+                }
+                if (row < row_end) left += (u32)min(P.n - row * 32, (u64)32);
+            }
+#pragma unroll
+            for (int b = 0; b < kBatch; ++b) issue(r + kRing + b, row_end, row0);
             n_valid += left;
-            process_batch<kNarrow>(g, t, ra, w, st, lane, lane_bit, lt_mask);
+            process_batch<kNarrow>(g, t, cur, w, st, lane, lane_bit, lt_mask);
             if (st.pot >= P.budget) {
-                if (left_n) record_partial(seg, pn / 32);
+                if (r + kBatch < row_end) record_partial(seg, r + kBatch);
                 stopped = true;
                 break;
             }
-            if (!left_n) break;
-            p0 = pn;
-            left = left_n;
-            pn = p0 + 32 * kBatch;
-            left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kBatch)) : 0u;
-            if (left_n) load_rows<kAligned>(P.xy, pn, left_n, lane, pol, ra);
-            n_valid += left;
-            process_batch<kNarrow>(g, t, rb, w, st, lane, lane_bit, lt_mask);
-            if (st.pot >= P.budget) {
-                if (left_n) record_partial(seg, pn / 32);
-                stopped = true;
-                break;
-            }
-            if (!left_n) break;
-            p0 = pn;
-            left = left_n;
         }
         if (stopped) {
             // hand back the prefetched ticket too
@@ -328,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         }
         have = fetch(seg, row0, from_ticket);
     }
+    cp_async_wait<0>();
 
     // Write back staged entries and the cache.
     flush_stage(t, w, st, lane);
@@ -497,6 +534,7 @@ int contract_max_warps(int n_sm) {
 }
 
 int contract_batch_rows() { return kBatch; }
+int contract_block_warps() { return kWarpsPerBlock; }
 
 cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     K1Params P;

@@ -24,6 +24,7 @@ struct ContractLaunch {
 
 int contract_max_warps(int n_sm);
 int contract_batch_rows();
+int contract_block_warps();
 cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st);
 cudaError_t launch_table_clear(Slot* slots, u64 n, int n_sm, cudaStream_t st);
 cudaError_t launch_table_fold(const Slot* src, u64 n_src, Table dst, u64* claimed, int n_sm,
