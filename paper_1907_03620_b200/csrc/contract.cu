@@ -145,7 +145,7 @@ struct K1State {
     u32 pot;      // warp-uniform: claimed keys + occupied cache entries + staged entries
     u32 slen;     // warp-uniform: staged entries
     u32 claims;   // per lane: keys this lane claimed in the table
-    u32 n_in;     // per lane: in-bounds points
+    u64 added;    // per lane: points this lane added to the table (= ingested, by conservation)
 };
 
 // Flush the staging list with every lane active: one table_add per entry,
@@ -153,7 +153,10 @@ struct K1State {
 // once per 32 misses instead of once per row).
 __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State& s, int lane) {
     u32 c = 0;
-    for (u32 e = lane; e < s.slen; e += 32) c += table_add(t, w.skey[e], w.scnt[e]) ? 1u : 0u;
+    for (u32 e = lane; e < s.slen; e += 32) {
+        c += table_add(t, w.skey[e], w.scnt[e]) ? 1u : 0u;
+        s.added += w.scnt[e];
+    }
     const u32 claimed = __reduce_add_sync(kFull, c);
     s.claims += c;
     s.pot = s.pot - s.slen + claimed;
@@ -171,7 +174,6 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
         inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
-        s.n_in += inb[b];
         // Computed unconditionally (no branch): for out-of-bounds or NaN
         // lanes the conversion result is meaningless and replaced by EMPTY.
         const u64 k = key_of<kNarrow>(g, cur.x[b], cur.y[b]);
@@ -187,13 +189,9 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
         const u64 cnt = __popc(peers[b]);
         // Hit: the slot holds this key. Distinct keys never hit the same
         // slot, so hitting leaders add without arbitration.
-        bool miss = false;
-        if (leader) {
-            if (w.ckey[cs] == key[b])
-                w.ccnt[cs] += cnt;
-            else
-                miss = true;
-        }
+        const bool hit = leader && w.ckey[cs] == key[b];
+        if (hit) w.ccnt[cs] += cnt;
+        const bool miss = leader && !hit;
         const u32 missmask = __ballot_sync(kFull, miss);
         if (missmask) {
             // One missing leader per slot installs its key; the slot's old
@@ -242,7 +240,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 #ifndef RG_K1_RING
-#define RG_K1_RING 8
+#define RG_K1_RING 4
 #endif
 constexpr int kRing = RG_K1_RING;  // rows in flight per warp (multiple of kBatch)
 
@@ -370,12 +368,19 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
     flush_stage(t, w, st, lane);
     for (int i = lane; i < kCacheSlots; i += 32) {
         const u64 k = w.ckey[i];
-        if (k != kEmpty) st.claims += table_add(t, k, w.ccnt[i]) ? 1u : 0u;
+        if (k != kEmpty) {
+            st.claims += table_add(t, k, w.ccnt[i]) ? 1u : 0u;
+            st.added += w.ccnt[i];
+        }
     }
 
-    // Counters: one atomic per warp.
+    // Counters: one atomic per warp. Every in-bounds point reached the table
+    // through exactly one table_add, so the added counts are the ingested
+    // points (conservation, test_accumulator.cpp:88-99).
     const u32 wc = __reduce_add_sync(kFull, st.claims);
-    const u64 wi = __reduce_add_sync(kFull, st.n_in);
+    u64 wi = st.added;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wi += __shfl_xor_sync(kFull, wi, o);
     if (lane == 0) {
         if (wi) atomicAdd(&P.ctr->ingested, wi);
         if (n_valid > wi) atomicAdd(&P.ctr->skipped, n_valid - wi);
