@@ -121,15 +121,8 @@ __device__ __forceinline__ void window_sync() {
         __syncthreads();
 }
 
-struct EdgeList {
-    uint2* e;       // deferred window-external edges (local root, neighbour)
-    u64 cap;
-    u64* n;         // device counter
-};
-
 __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
-                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent,
-                                               EdgeList el) {
+                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent) {
     __shared__ u32 s_par[256];
     const u64 n_sig = *n_sig_p;
     const u32 loc = threadIdx.x % kUnionWindow;
@@ -185,41 +178,12 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
             const u32 target = (u32)base + r;  // < i: keeps parent[x] <= x
             if (atomicCAS(parent + i, (u32)i, target) != (u32)i) uf_unite(parent, (u32)i, target);
         }
-        // Edges leaving the window are deferred to k_union_edges, which runs
-        // once every window has linked its tiles to their local roots (finds
-        // are then short and no window races a half-built one). An edge is
-        // recorded from the local root, and duplicates from the same lane are
-        // dropped; if the list is full the edge is united here.
-        u32 prev = 0xffffffffu;
+        // edges leaving the window
 #pragma unroll
-        for (int o = 0; o < kStoredNb; ++o) {
-            const u32 j = nb[o];
-            const bool ext = j != 0xffffffffu && (j < base || j >= base + kUnionWindow) && j != prev;
-            const u32 m = __ballot_sync(kFull, ext);
-            if (m) {
-                u64 at = 0;
-                if ((threadIdx.x & 31) == 0) at = atomicAdd(el.n, (u64)__popc(m));
-                at = __shfl_sync(kFull, at, 0) + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
-                if (ext) {
-                    if (at < el.cap)
-                        el.e[at] = make_uint2((u32)base + r, j);
-                    else
-                        uf_unite(parent, (u32)i, j);
-                }
-            }
-            if (j != 0xffffffffu) prev = j;
-        }
+        for (int o = 0; o < kStoredNb; ++o)
+            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + kUnionWindow))
+                uf_unite(parent, (u32)i, nb[o]);
         window_sync();
-    }
-}
-
-// Deferred window-external edges.
-__global__ void k_union_edges(const uint2* e, const u64* n_p, u64 cap, u32* parent) {
-    const u64 n = min(*n_p, cap);
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x) {
-        const uint2 v = e[i];
-        uf_unite(parent, v.x, v.y);
     }
 }
 
@@ -371,10 +335,7 @@ static int grid_for(u64 n, int n_sm, int per_sm = 8) {
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     const int gs = grid_for(A.n_sig, A.n_sm, 16);
     Offsets off{A.offsets, A.n_offsets, A.cheb1};
-    const EdgeList el{A.edges, A.edge_cap, &A.ctr->n_edges};
-    cudaMemsetAsync(&A.ctr->n_edges, 0, sizeof(u64), st);
-    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent, el);
-    k_union_edges<<<gs, 256, 0, st>>>(A.edges, &A.ctr->n_edges, A.edge_cap, A.parent);
+    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent);
     k_compress_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size,
                                           A.npts, A.min_key);
     k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,

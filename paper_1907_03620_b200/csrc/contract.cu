@@ -189,19 +189,9 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
         const u64 cnt = __popc(peers[b]);
         // Hit: the slot holds this key. Distinct keys never hit the same
         // slot, so hitting leaders add without arbitration.
-#ifdef RG_HIT_BRANCH
-        bool miss = false;
-        if (leader) {
-            if (w.ckey[cs] == key[b])
-                w.ccnt[cs] += cnt;
-            else
-                miss = true;
-        }
-#else
         const bool hit = leader && w.ckey[cs] == key[b];
         if (hit) w.ccnt[cs] += cnt;
         const bool miss = leader && !hit;
-#endif
         const u32 missmask = __ballot_sync(kFull, miss);
         if (missmask) {
             // One missing leader per slot installs its key; the slot's old
