@@ -121,9 +121,18 @@ __device__ __forceinline__ void window_sync() {
         __syncthreads();
 }
 
+struct EdgeList {
+    uint2* e;  // deferred window-external edges (local root, neighbour)
+    u64 cap;
+    u64* n;    // device counter
+};
+
 __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
-                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent) {
+                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent,
+                                               EdgeList el) {
     __shared__ u32 s_par[256];
+    __shared__ u32 s_wsum[8];
+    __shared__ u64 s_base;
     const u64 n_sig = *n_sig_p;
     const u32 loc = threadIdx.x % kUnionWindow;
     u32* lp = s_par + (threadIdx.x - loc);
@@ -178,12 +187,62 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
             const u32 target = (u32)base + r;  // < i: keeps parent[x] <= x
             if (atomicCAS(parent + i, (u32)i, target) != (u32)i) uf_unite(parent, (u32)i, target);
         }
-        // edges leaving the window
+        // Edges leaving the window are deferred to k_union_edges, which runs
+        // once every window has linked its tiles to their local roots (finds
+        // are then short, and the divergent per-lane union loops become one
+        // uniform thread per edge). Edges are recorded from the local root;
+        // the block reserves its list space with one atomic. If the list is
+        // full the edge is united here.
+        u32 ext = 0;
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + kUnionWindow))
-                uf_unite(parent, (u32)i, nb[o]);
-        window_sync();
+            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + kUnionWindow)) {
+                bool dup = false;
+#pragma unroll
+                for (int q = 0; q < o; ++q) dup |= nb[q] == nb[o];
+                if (!dup) ext |= 1u << o;
+            }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const u32 cnt = __popc(ext);
+        u32 incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) s_wsum[wid] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u32 tot = 0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+                const u32 c = s_wsum[q];
+                s_wsum[q] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(el.n, (u64)tot) : 0;
+        }
+        __syncthreads();
+        u64 at = s_base + s_wsum[wid] + incl - cnt;
+#pragma unroll
+        for (int o = 0; o < kStoredNb; ++o)
+            if (ext >> o & 1) {
+                if (at < el.cap)
+                    el.e[at] = make_uint2((u32)base + r, nb[o]);
+                else
+                    uf_unite(parent, (u32)i, nb[o]);
+                ++at;
+            }
+        __syncthreads();
+    }
+}
+
+// Deferred window-external edges: one thread per edge.
+__global__ void k_union_edges(const uint2* e, const u64* n_p, u64 cap, u32* parent) {
+    const u64 n = min(*n_p, cap);
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const uint2 v = e[i];
+        uf_unite(parent, v.x, v.y);
     }
 }
 
@@ -335,7 +394,10 @@ static int grid_for(u64 n, int n_sm, int per_sm = 8) {
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     const int gs = grid_for(A.n_sig, A.n_sm, 16);
     Offsets off{A.offsets, A.n_offsets, A.cheb1};
-    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent);
+    const EdgeList el{A.edges, A.edge_cap, &A.ctr->n_edges};
+    cudaMemsetAsync(&A.ctr->n_edges, 0, sizeof(u64), st);
+    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent, el);
+    k_union_edges<<<gs, 256, 0, st>>>(A.edges, &A.ctr->n_edges, A.edge_cap, A.parent);
     k_compress_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size,
                                           A.npts, A.min_key);
     k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,

@@ -166,6 +166,8 @@ struct rg_ctx {
     int *tile_cid = nullptr, *root_cid = nullptr;
     u64 *root_key = nullptr, *root_key_sorted = nullptr;
     u32 *root_idx = nullptr, *root_idx_sorted = nullptr;
+    uint2* edges = nullptr;  // K3 deferred edges, capacity edge_cap
+    u64 edge_cap = 0;
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -622,7 +624,9 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     dfree(ctx->root_key_sorted);
     dfree(ctx->root_idx);
     dfree(ctx->root_idx_sorted);
+    dfree(ctx->edges);
     ctx->sig_cap = 0;
+    ctx->edge_cap = 0;
     const u64 c = std::max<u64>(n, 1024);
     CK(dalloc(&ctx->sig_key, c));
     CK(dalloc(&ctx->sig_cnt, c));
@@ -636,6 +640,8 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     CK(dalloc(&ctx->root_key_sorted, c));
     CK(dalloc(&ctx->root_idx, c));
     CK(dalloc(&ctx->root_idx_sorted, c));
+    CK(dalloc(&ctx->edges, c));  // overflow edges are united in place
+    ctx->edge_cap = c;
     ctx->sig_cap = c;
     return RG_OK;
 }
@@ -718,12 +724,14 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
     A.root_idx = ctx->root_idx;
     A.root_key_sorted = ctx->root_key_sorted;
     A.root_idx_sorted = ctx->root_idx_sorted;
+    A.edges = ctx->edges;
+    A.edge_cap = ctx->edge_cap;
     A.ctr = ctx->ctr;
     A.n_sm = ctx->n_sm;
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);
     CK(launch_agglomerate(A, ctx->st));
-    ctx->launches += 3;
+    ctx->launches += 4;
     CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
                        cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -932,6 +940,7 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->root_key_sorted);
     dfree(ctx->root_idx);
     dfree(ctx->root_idx_sorted);
+    dfree(ctx->edges);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {

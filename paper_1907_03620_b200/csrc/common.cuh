@@ -206,7 +206,8 @@ struct Counters {
     u64 n_roots;         // components
     u64 n_kept;          // clusters after the mu filter
     u64 first_oob;       // strict policy: smallest out-of-bounds index
-    u64 pad2[12];
+    u64 n_edges;         // deferred union edges (K3)
+    u64 pad2[11];
 };
 
 struct Partial {

@@ -52,6 +52,8 @@ struct AggLaunch {
     u64* min_key;
     int* root_cid;
     int* tile_cid;
+    uint2* edges;     // deferred external edges of k_union
+    u64 edge_cap;
     u64* root_key;
     u32* root_idx;
     u64* root_key_sorted;
