@@ -80,35 +80,6 @@ __device__ __forceinline__ u32 sig_index(const Table& t, long long kx, long long
     return (v != kEmpty && (v & kSigBit)) ? (u32)(v & ~kSigBit) : 0xffffffffu;
 }
 
-// Four neighbour lookups with their first loads in flight together (the
-// lookups are latency-bound: random buckets, short chains), each finished by
-// its own probe loop only when the first slot holds a different key.
-__device__ __forceinline__ void sig_index4(const Table& t, long long kx, long long ky,
-                                           const int2 (&d)[4], u32 bits_y, long long xlim,
-                                           long long ylim, u32 (&out)[4]) {
-    u64 key[4], k[4], v[4];
-    Probe pr[4] = {Probe(0, t), Probe(0, t), Probe(0, t), Probe(0, t)};
-    bool ok[4];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-        const long long nx = kx + d[o].x, ny = ky + d[o].y;
-        ok[o] = !(nx < 0 || nx >= xlim || ny < 0 || ny >= ylim);
-        key[o] = ((u64)nx << bits_y) | (u64)ny;
-        pr[o] = Probe(key[o], t);
-        if (ok[o]) ld_slot(t.slots + pr[o].slot(), k[o], v[o]);
-    }
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-        out[o] = 0xffffffffu;
-        if (!ok[o]) continue;
-        while (k[o] != key[o] && k[o] != kEmpty) {
-            pr[o].next(t);
-            ld_slot(t.slots + pr[o].slot(), k[o], v[o]);
-        }
-        if (k[o] == key[o] && (v[o] & kSigBit)) out[o] = (u32)(v[o] & ~kSigBit);
-    }
-}
-
 __device__ __forceinline__ u32 lfind(volatile u32* lp, u32 x) {
     u32 p;
     while ((p = lp[x]) != x) x = p;
@@ -186,11 +157,12 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
                 // own forward probes make the diagonal edge redundant, so the
                 // diagonals are probed only when needed (fewer unsuccessful
                 // probes, the long ones).
-                const int2 d4[4] = {make_int2(0, 1), make_int2(1, -1), make_int2(1, 0),
-                                    make_int2(1, 1)};
-                sig_index4(t, kx, ky, d4, bits_y, xlim, ylim, nb);
-                if (nb[2] != 0xffffffffu) nb[1] = 0xffffffffu;
-                if (nb[0] != 0xffffffffu || nb[2] != 0xffffffffu) nb[3] = 0xffffffffu;
+                nb[0] = sig_index(t, kx, ky, 0, 1, bits_y, xlim, ylim);
+                nb[2] = sig_index(t, kx, ky, 1, 0, bits_y, xlim, ylim);
+                if (nb[2] == 0xffffffffu) {
+                    nb[1] = sig_index(t, kx, ky, 1, -1, bits_y, xlim, ylim);
+                    if (nb[0] == 0xffffffffu) nb[3] = sig_index(t, kx, ky, 1, 1, bits_y, xlim, ylim);
+                }
             } else {
                 for (int o = 0; o < off.n; ++o) {
                     const int2 d = off.d[o];
