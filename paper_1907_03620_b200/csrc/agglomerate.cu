@@ -72,14 +72,11 @@ struct Offsets {
 };
 
 // Significant-tile index of (kx+dx, ky+dy), or 0xffffffff.
-__device__ __forceinline__ u32 sig_index(const Table& t, const SigTable& st, long long kx,
-                                         long long ky, int dx, int dy, u32 bits_y, long long xlim,
-                                         long long ylim) {
+__device__ __forceinline__ u32 sig_index(const Table& t, long long kx, long long ky, int dx, int dy,
+                                         u32 bits_y, long long xlim, long long ylim) {
     const long long nx = kx + dx, ny = ky + dy;
     if (nx < 0 || nx >= xlim || ny < 0 || ny >= ylim) return 0xffffffffu;
-    const u64 key = ((u64)nx << bits_y) | (u64)ny;
-    if (st.on) return stab_find(st, key);
-    const u64 v = table_find(t, key);
+    const u64 v = table_find(t, ((u64)nx << bits_y) | (u64)ny);
     return (v != kEmpty && (v & kSigBit)) ? (u32)(v & ~kSigBit) : 0xffffffffu;
 }
 
@@ -131,8 +128,8 @@ struct EdgeList {
 };
 
 __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
-                                               SigTable stab, u32 bits_y, u32 bits_x, Offsets off,
-                                               u32* parent, EdgeList el) {
+                                               u32 bits_y, u32 bits_x, Offsets off, u32* parent,
+                                               EdgeList el) {
     __shared__ u32 s_par[256];
     __shared__ u32 s_wsum[8];
     __shared__ u64 s_base;
@@ -160,16 +157,16 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
                 // own forward probes make the diagonal edge redundant, so the
                 // diagonals are probed only when needed (fewer unsuccessful
                 // probes, the long ones).
-                nb[0] = sig_index(t, stab, kx, ky, 0, 1, bits_y, xlim, ylim);
-                nb[2] = sig_index(t, stab, kx, ky, 1, 0, bits_y, xlim, ylim);
+                nb[0] = sig_index(t, kx, ky, 0, 1, bits_y, xlim, ylim);
+                nb[2] = sig_index(t, kx, ky, 1, 0, bits_y, xlim, ylim);
                 if (nb[2] == 0xffffffffu) {
-                    nb[1] = sig_index(t, stab, kx, ky, 1, -1, bits_y, xlim, ylim);
-                    if (nb[0] == 0xffffffffu) nb[3] = sig_index(t, stab, kx, ky, 1, 1, bits_y, xlim, ylim);
+                    nb[1] = sig_index(t, kx, ky, 1, -1, bits_y, xlim, ylim);
+                    if (nb[0] == 0xffffffffu) nb[3] = sig_index(t, kx, ky, 1, 1, bits_y, xlim, ylim);
                 }
             } else {
                 for (int o = 0; o < off.n; ++o) {
                     const int2 d = off.d[o];
-                    const u32 j = sig_index(t, stab, kx, ky, d.x, d.y, bits_y, xlim, ylim);
+                    const u32 j = sig_index(t, kx, ky, d.x, d.y, bits_y, xlim, ylim);
                     if (j == 0xffffffffu) continue;
                     if (o < kStoredNb)
                         nb[o] = j;
@@ -368,9 +365,9 @@ __global__ void k_label_tiles(const u32* parent, const int* root_cid, const u64*
 // Load path (agglomerate(SignificantTiles) with caller tiles): pack and insert
 // every tile as significant with its dense index.
 __global__ void k_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
-                             long long ox, long long oy, u32 bits_y, Table t, SigTable stab,
-                             u64* sig_key, u64* sig_cnt, u32* parent, u32* size, u64* npts,
-                             u64* min_key, int* root_cid) {
+                             long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                             u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                             int* root_cid) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x) {
         const u64 key = ((u64)(tx[i] - ox) << bits_y) | (u64)(ty[i] - oy);
@@ -383,7 +380,6 @@ __global__ void k_load_tiles(const long long* tx, const long long* ty, const u64
         root_cid[i] = -1;
         const u64 slot = table_claim(t, key);
         t.slots[slot].count = kSigBit | i;
-        if (stab.on) stab_insert(stab, key, i);
     }
 }
 
@@ -400,8 +396,7 @@ cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     Offsets off{A.offsets, A.n_offsets, A.cheb1};
     const EdgeList el{A.edges, A.edge_cap, &A.ctr->n_edges};
     cudaMemsetAsync(&A.ctr->n_edges, 0, sizeof(u64), st);
-    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.stab, A.bits_y, A.bits_x, off,
-                                A.parent, el);
+    k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent, el);
     k_union_edges<<<gs, 256, 0, st>>>(A.edges, &A.ctr->n_edges, A.edge_cap, A.parent);
     k_compress_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size,
                                           A.npts, A.min_key);
@@ -440,12 +435,12 @@ cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_ou
 }
 
 cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
-                              long long ox, long long oy, u32 bits_y, Table t, SigTable stab,
-                              u64* sig_key, u64* sig_cnt, u32* parent, u32* size, u64* npts,
-                              u64* min_key, int* root_cid, int n_sm, cudaStream_t st) {
-    k_load_tiles<<<grid_for(n, n_sm), 256, 0, st>>>(tx, ty, cnt, n, ox, oy, bits_y, t, stab,
-                                                     sig_key, sig_cnt, parent, size, npts,
-                                                     min_key, root_cid);
+                              long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                              u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                              int* root_cid, int n_sm, cudaStream_t st) {
+    k_load_tiles<<<grid_for(n, n_sm), 256, 0, st>>>(tx, ty, cnt, n, ox, oy, bits_y, t, sig_key,
+                                                     sig_cnt, parent, size, npts, min_key,
+                                                     root_cid);
     return cudaGetLastError();
 }
 

@@ -167,9 +167,6 @@ struct rg_ctx {
     u64 *root_key = nullptr, *root_key_sorted = nullptr;
     u32 *root_idx = nullptr, *root_idx_sorted = nullptr;
     uint2* edges = nullptr;  // K3 deferred edges, capacity edge_cap
-    u64* stab = nullptr;     // significant-tile index (SigTable), stab_cap slots
-    u64 stab_cap = 0;
-    SigTable stab_view{};    // current view (on = 0 when unusable)
     u64 edge_cap = 0;
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
@@ -316,32 +313,6 @@ Table make_table(Slot* slots, u64 cap, u32 bits_y) {
 }
 
 Table table_of(const rg_ctx* c) { return make_table(c->slots, c->cap, c->res.bits_y); }
-
-// Prepare the significant-tile index for up to n_max entries (cleared). It is
-// disabled (on = 0) when key bits + index bits would exceed 64.
-rg_status prepare_stab(rg_ctx* ctx, u64 n_max) {
-    ctx->stab_view = SigTable{};
-    const u64 cap = next_pow2(std::max<u64>((u64)((double)n_max / 0.75) + 1, 1024));
-    const u32 ib = log2u(cap);
-    const u32 kb = ctx->res.bits_x + ctx->res.bits_y;
-    if (kb + ib > 64) return RG_OK;
-    if (ctx->stab_cap < cap) {
-        dfree(ctx->stab);
-        ctx->stab_cap = 0;
-        CK(dalloc(&ctx->stab, cap));
-        ctx->stab_cap = cap;
-    }
-    CK(cudaMemsetAsync(ctx->stab, 0xff, cap * sizeof(u64), ctx->st));
-    SigTable st;
-    st.e = ctx->stab;
-    st.bmask = cap / kBucketSlots - 1;
-    st.shift = 64 - log2u(cap / kBucketSlots);
-    st.bits_y = ctx->res.bits_y;
-    st.ib = ib;
-    st.on = 1;
-    ctx->stab_view = st;
-    return RG_OK;
-}
 
 rg_status alloc_table(rg_ctx* ctx, u64 cap, Slot** out) {
     CK(dalloc(out, cap));
@@ -695,13 +666,10 @@ rg_status prune_impl(rg_ctx* ctx) {
     if (s != RG_OK) return s;
     PhaseTimer timer(ctx, &ctx->ms_prune);
     zero_field(ctx, &ctx->ctr->n_sig);
-    ctx->res = ctx->grid;
-    s = prepare_stab(ctx, ctx->used);  // S <= D = used
-    if (s != RG_OK) return s;
     if (ctx->slots && ctx->used) {
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
-                          ctx->parent, ctx->size, ctx->npts, ctx->min_key, ctx->root_cid,
-                          ctx->stab_view, ctx->ctr, ctx->n_sm, ctx->st));
+                          ctx->parent, ctx->size, ctx->npts, ctx->min_key, ctx->root_cid, ctx->ctr,
+                          ctx->n_sm, ctx->st));
         ++ctx->launches;
     }
     CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, sizeof(u64), cudaMemcpyDeviceToHost,
@@ -740,7 +708,6 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
     A.n_sig_dev = &ctx->ctr->n_sig;
     A.n_sig = ctx->n_sig;
     A.t = table_of(ctx);
-    A.stab = ctx->stab_view;
     A.bits_y = ctx->res.bits_y;
     A.bits_x = ctx->res.bits_x;
     A.offsets = ctx->offsets;
@@ -974,7 +941,6 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->root_idx);
     dfree(ctx->root_idx_sorted);
     dfree(ctx->edges);
-    dfree(ctx->stab);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {
@@ -1202,8 +1168,6 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     ctx->res = res;  // the table is keyed with this packing
     s = ensure_sig_capacity(ctx, n);
     if (s != RG_OK) return s;
-    s = prepare_stab(ctx, n);
-    if (s != RG_OK) return s;
     if (n) {
         long long *dtx = nullptr, *dty = nullptr;
         u64* dcnt = nullptr;
@@ -1216,9 +1180,8 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
         CK(cudaMemcpyAsync(dty, ty, n * 8, mk, ctx->st));
         if (count) CK(cudaMemcpyAsync(dcnt, count, n * 8, mk, ctx->st));
         CK(launch_load_tiles(dtx, dty, dcnt, n, res.origin_x, res.origin_y, res.bits_y,
-                             table_of(ctx), ctx->stab_view, ctx->sig_key, ctx->sig_cnt,
-                             ctx->parent, ctx->size, ctx->npts, ctx->min_key, ctx->root_cid,
-                             ctx->n_sm, ctx->st));
+                             table_of(ctx), ctx->sig_key, ctx->sig_cnt, ctx->parent, ctx->size,
+                             ctx->npts, ctx->min_key, ctx->root_cid, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
         dfree(dtx);
@@ -1429,8 +1392,7 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         return RG_OK;
     }
     if (kind == RG_MEM_DEVICE) {
-        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->stab_view, ctx->tile_cid,
-                               labels, ctx->narrow,
+        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, labels, ctx->narrow,
                                ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
@@ -1444,8 +1406,7 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         const u64 len = std::min(ch, n - off);
         CK(cudaMemcpyAsync(ctx->stage[b], xy + 2 * off, len * 16, cudaMemcpyHostToDevice,
                            ctx->st));
-        CK(launch_label_points(ctx->stage[b], len, ctx->grid, table_of(ctx), ctx->stab_view,
-                               ctx->tile_cid,
+        CK(launch_label_points(ctx->stage[b], len, ctx->grid, table_of(ctx), ctx->tile_cid,
                                ctx->lstage[b], ctx->narrow, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaMemcpyAsync(labels + off, ctx->lstage[b], len * 4, cudaMemcpyDeviceToHost,

@@ -77,8 +77,7 @@ struct Table {
 struct Probe {
     u64 b0, b;
     u32 pos;
-    template <typename T>
-    __device__ __forceinline__ Probe(u64 key, const T& t) {
+    __device__ __forceinline__ Probe(u64 key, const Table& t) {
         const u64 ky = key & ((1ull << t.bits_y) - 1);
         const u64 block =
             ((key >> (t.bits_y + kBlockBits)) << (t.bits_y - kBlockBits)) | (ky >> kBlockBits);
@@ -89,8 +88,7 @@ struct Probe {
         pos = ((kx << kBlockBits) | kyl) ^ ((u32)(h >> (t.shift - 2 * kBlockBits)) & (kBucketSlots - 1));
     }
     __device__ __forceinline__ u64 slot() const { return (b << (2 * kBlockBits)) | pos; }
-    template <typename T>
-    __device__ __forceinline__ void next(const T& t) {
+    __device__ __forceinline__ void next(const Table& t) {
         b = (b + 1) & t.bmask;
         if (b == b0) pos = (pos + 1) & (kBucketSlots - 1);
     }
@@ -189,42 +187,6 @@ __device__ __forceinline__ u64 table_claim(const Table& t, u64 key) {
         const u64 old = atomicCAS(&t.slots[i].key, kEmpty, key);
         if (old == kEmpty || old == key) return i;
         p.next(t);
-    }
-}
-
-// Significant-tile index. Built by K2 next to the dense arrays: one 8-byte
-// entry (key << ib | dense index) per significant tile, in the same
-// block-bucketed layout as the counting table (a 16-slot bucket is one
-// 128-byte line). It holds only S entries at load <= 0.75, so agglomeration's
-// neighbour probes and the labelling pass hit a footprint that mostly fits
-// in L2 instead of the counting table's HBM-resident one.
-struct SigTable {
-    u64* e;
-    u64 bmask;
-    u32 shift;
-    u32 bits_y;
-    u32 ib;  // index bits
-    u32 on;  // 0: key bits + index bits exceed 64 -> use the counting table
-};
-
-__device__ __forceinline__ void stab_insert(const SigTable& s, u64 key, u64 idx) {
-    const u64 entry = (key << s.ib) | idx;
-    Probe p(key, s);
-    while (true) {
-        if (atomicCAS(s.e + p.slot(), kEmpty, entry) == kEmpty) return;
-        p.next(s);
-    }
-}
-
-// Dense index of a significant tile, or 0xffffffff.
-__device__ __forceinline__ u32 stab_find(const SigTable& s, u64 key) {
-    Probe p(key, s);
-    while (true) {
-        u64 v;
-        asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(s.e + p.slot()));
-        if (v == kEmpty) return 0xffffffffu;
-        if ((v >> s.ib) == key) return (u32)(v & ((1ull << s.ib) - 1));
-        p.next(s);
     }
 }
 

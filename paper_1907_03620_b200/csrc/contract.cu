@@ -448,7 +448,6 @@ struct K2Out {
     u64* npts;
     u64* min_key;
     int* root_cid;
-    SigTable stab;
 };
 
 __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n, const K2Out& o,
@@ -469,7 +468,6 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
         o.min_key[pos] = kEmpty;
         o.root_cid[pos] = -1;
         t.slots[i].count = kSigBit | pos;
-        if (o.stab.on) stab_insert(o.stab, k, pos);
     }
     __syncwarp();
 }
@@ -594,12 +592,12 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 }
 
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           u32* size, u64* npts, u64* min_key, int* root_cid, SigTable stab,
-                           Counters* ctr, int n_sm, cudaStream_t st) {
+                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
+                           int n_sm, cudaStream_t st) {
     const u64 per_block = 256ull * kK2Items;
     const u64 want = (cap + per_block - 1) / per_block;
     const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
-    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid, stab};
+    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid};
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, o, ctr);
     return cudaGetLastError();
 }

@@ -32,8 +32,8 @@ cudaError_t launch_table_fold(const Slot* src, u64 n_src, Table dst, u64* claime
 cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           u32* size, u64* npts, u64* min_key, int* root_cid, SigTable stab,
-                           Counters* ctr, int n_sm, cudaStream_t st);
+                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
+                           int n_sm, cudaStream_t st);
 
 struct AggLaunch {
     const u64* sig_key;
@@ -41,7 +41,6 @@ struct AggLaunch {
     const u64* n_sig_dev;  // device copy of S (&ctr->n_sig)
     u64 n_sig;             // host copy of S (for sizing)
     Table t;
-    SigTable stab;
     u32 bits_y, bits_x;
     const int2* offsets;
     int n_offsets;
@@ -71,13 +70,12 @@ size_t sort_pairs_temp_bytes(u64 n, int bits);
 cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_out,
                        const u32* v_in, u32* v_out, u64 n, int bits, cudaStream_t st);
 cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u64* cnt, u64 n,
-                              long long ox, long long oy, u32 bits_y, Table t, SigTable stab,
-                              u64* sig_key, u64* sig_cnt, u32* parent, u32* size, u64* npts,
-                              u64* min_key, int* root_cid, int n_sm, cudaStream_t st);
+                              long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
+                              u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
+                              int* root_cid, int n_sm, cudaStream_t st);
 
-cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, SigTable stab,
-                                const int* tile_cid, int* labels, bool narrow, int n_sm,
-                                cudaStream_t st);
+cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
+                                int* labels, bool narrow, int n_sm, cudaStream_t st);
 
 // small utility kernels (api.cu)
 cudaError_t launch_iota(u32* out, u64 n, int n_sm, cudaStream_t st);

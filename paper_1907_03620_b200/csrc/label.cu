@@ -82,8 +82,7 @@ __device__ __forceinline__ u64 l_key(const Grid& g, double x, double y) {
 }
 
 template <bool kNarrow>
-__device__ __forceinline__ void l_batch(const Grid& g, const Table& t, const SigTable& stab,
-                                        const int* tile_cid,
+__device__ __forceinline__ void l_batch(const Grid& g, const Table& t, const int* tile_cid,
                                         const LRows& cur, u64 p0, u32 left, LSmem& w, int lane,
                                         u32 lane_bit, int* labels) {
 #pragma unroll
@@ -105,13 +104,8 @@ __device__ __forceinline__ void l_batch(const Grid& g, const Table& t, const Sig
         }
         if (__any_sync(kFull, miss)) {
             if (miss) {
-                if (stab.on) {
-                    const u32 j = stab_find(stab, key);
-                    cid = j != 0xffffffffu ? tile_cid[j] : -1;
-                } else {
-                    const u64 v = table_find(t, key);
-                    cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
-                }
+                const u64 v = table_find(t, key);
+                cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
                 w.owner[cs] = (unsigned char)lane;
             }
             __syncwarp();
@@ -128,8 +122,7 @@ __device__ __forceinline__ void l_batch(const Grid& g, const Table& t, const Sig
 
 template <bool kAligned, bool kNarrow>
 __global__ void __launch_bounds__(kLWarps * 32) k_label_points(const double* xy, u64 n, Grid g,
-                                                               Table t, SigTable stab,
-                                                               const int* tile_cid,
+                                                               Table t, const int* tile_cid,
                                                                int* labels) {
     __shared__ LSmem s_warp[kLWarps];
     const int lane = threadIdx.x & 31;
@@ -152,14 +145,14 @@ __global__ void __launch_bounds__(kLWarps * 32) k_label_points(const double* xy,
             u64 pn = p0 + 32 * kLBatch;
             u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kLBatch)) : 0u;
             if (left_n) l_load<kAligned>(xy, pn, left_n, lane, pol, rb);
-            l_batch<kNarrow>(g, t, stab, tile_cid, ra, p0, left, w, lane, lane_bit, labels);
+            l_batch<kNarrow>(g, t, tile_cid, ra, p0, left, w, lane, lane_bit, labels);
             if (!left_n) break;
             p0 = pn;
             left = left_n;
             pn = p0 + 32 * kLBatch;
             left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kLBatch)) : 0u;
             if (left_n) l_load<kAligned>(xy, pn, left_n, lane, pol, ra);
-            l_batch<kNarrow>(g, t, stab, tile_cid, rb, p0, left, w, lane, lane_bit, labels);
+            l_batch<kNarrow>(g, t, tile_cid, rb, p0, left, w, lane, lane_bit, labels);
             if (!left_n) break;
             p0 = pn;
             left = left_n;
@@ -169,9 +162,8 @@ __global__ void __launch_bounds__(kLWarps * 32) k_label_points(const double* xy,
 
 static int g_label_blocks_per_sm = 0;
 
-cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, SigTable stab,
-                                const int* tile_cid, int* labels, bool narrow, int n_sm,
-                                cudaStream_t st) {
+cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
+                                int* labels, bool narrow, int n_sm, cudaStream_t st) {
     if (!g_label_blocks_per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_label_blocks_per_sm,
                                                       k_label_points<true, false>, kLWarps * 32, 0);
@@ -185,13 +177,13 @@ cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, SigTab
     if (blocks == 0) blocks = 1;
     const bool aligned = ((uintptr_t)xy & 15) == 0;
     if (aligned && narrow)
-        k_label_points<true, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, stab, tile_cid, labels);
+        k_label_points<true, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
     else if (aligned)
-        k_label_points<true, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, stab, tile_cid, labels);
+        k_label_points<true, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
     else if (narrow)
-        k_label_points<false, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, stab, tile_cid, labels);
+        k_label_points<false, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
     else
-        k_label_points<false, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, stab, tile_cid, labels);
+        k_label_points<false, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
     return cudaGetLastError();
 }
 
