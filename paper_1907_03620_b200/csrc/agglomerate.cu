@@ -104,46 +104,70 @@ __device__ __forceinline__ void lunite(u32* lp, u32 a, u32 b) {
 
 constexpr int kStoredNb = 4;  // neighbour indices kept per tile for the warp-local pass
 
-// Union step. Tiles come in compaction (bucket) order, so a block's 256
-// consecutive tiles are mostly spatial neighbours: edges between them are
-// resolved first in a shared-memory union-find (cheap, no global contention),
-// each local component is then linked to its smallest member with one CAS,
-// and only edges leaving the window go through the global union-find.
-#ifndef RG_UNION_WINDOW
-#define RG_UNION_WINDOW 256
-#endif
-constexpr int kUnionWindow = RG_UNION_WINDOW;  // = blockDim.x
-
-__device__ __forceinline__ void window_sync() {
-    if (kUnionWindow == 32)
-        __syncwarp();
-    else
-        __syncthreads();
-}
-
+// Union step. Tiles come in compaction (bucket) order, so a warp's 32
+// consecutive tiles are mostly spatial neighbours. Each warp:
+//   1. probes the forward neighbours of its 32 tiles in the counting table
+//      (for Chebyshev delta 1 the two orthogonal probes are issued together
+//      and the diagonals only when needed — they are otherwise reached
+//      through the orthogonal neighbours);
+//   2. resolves edges between its own tiles with a shared-memory union-find
+//      over lanes and points every tile at its local component's smallest
+//      member (a plain store: no other thread writes these entries in this
+//      kernel, so nothing can be overwritten);
+//   3. writes the edges that leave the warp into the warp's fixed slots of
+//      the edge list (no atomics), for k_union_edges.
+// Global union-find work therefore runs once every tile is linked to its
+// local root (short finds) and as one uniform thread per edge, instead of as
+// divergent per-lane loops here.
 struct EdgeList {
-    uint2* e;  // deferred window-external edges (local root, neighbour)
-    u64 cap;
-    u64* n;    // device counter
+    uint2* e;    // kEdgeSlots per warp window
+    u32* n;      // edges per window
 };
+constexpr int kEdgeSlots = 32 * kStoredNb;
+
+// Two lookups with their first loads in flight together (latency-bound:
+// random buckets, short chains), each finished by its own probe loop only
+// when the first slot holds a different key.
+__device__ __forceinline__ void sig_index2(const Table& t, long long kx, long long ky, int2 d0,
+                                           int2 d1, u32 bits_y, long long xlim, long long ylim,
+                                           u32& o0, u32& o1) {
+    const long long x0 = kx + d0.x, y0 = ky + d0.y, x1 = kx + d1.x, y1 = ky + d1.y;
+    const bool ok0 = !(x0 < 0 || x0 >= xlim || y0 < 0 || y0 >= ylim);
+    const bool ok1 = !(x1 < 0 || x1 >= xlim || y1 < 0 || y1 >= ylim);
+    const u64 q0 = ((u64)x0 << bits_y) | (u64)y0, q1 = ((u64)x1 << bits_y) | (u64)y1;
+    Probe p0(q0, t), p1(q1, t);
+    u64 k0 = kEmpty, v0 = 0, k1 = kEmpty, v1 = 0;
+    if (ok0) ld_slot(t.slots + p0.slot(), k0, v0);
+    if (ok1) ld_slot(t.slots + p1.slot(), k1, v1);
+    while (ok0 && k0 != q0 && k0 != kEmpty) {
+        p0.next(t);
+        ld_slot(t.slots + p0.slot(), k0, v0);
+    }
+    while (ok1 && k1 != q1 && k1 != kEmpty) {
+        p1.next(t);
+        ld_slot(t.slots + p1.slot(), k1, v1);
+    }
+    o0 = (ok0 && k0 == q0 && (v0 & kSigBit)) ? (u32)(v0 & ~kSigBit) : 0xffffffffu;
+    o1 = (ok1 && k1 == q1 && (v1 & kSigBit)) ? (u32)(v1 & ~kSigBit) : 0xffffffffu;
+}
 
 __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_sig_p, Table t,
                                                u32 bits_y, u32 bits_x, Offsets off, u32* parent,
                                                EdgeList el) {
-    __shared__ u32 s_par[256];
-    __shared__ u32 s_wsum[8];
-    __shared__ u64 s_base;
+    __shared__ u32 s_par[8][32];
     const u64 n_sig = *n_sig_p;
-    const u32 loc = threadIdx.x % kUnionWindow;
-    u32* lp = s_par + (threadIdx.x - loc);
+    const int lane = threadIdx.x & 31;
+    u32* lp = s_par[threadIdx.x >> 5];
     const long long ymask = (1ll << bits_y) - 1;
     const long long xlim = 1ll << bits_x, ylim = 1ll << bits_y;
-    const u64 span = (n_sig + 255) / 256 * 256;
+    const bool wide = off.n > kStoredNb;  // some edges are united here (delta > 1)
+    const u64 span = (n_sig + 31) / 32 * 32;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
-        const u64 base = i - loc;
+        const u64 base = i - lane;
+        const u64 win = base / 32;
         const bool valid = i < n_sig;
-        lp[loc] = loc;
+        lp[lane] = lane;
         u32 nb[kStoredNb];
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o) nb[o] = 0xffffffffu;
@@ -152,16 +176,14 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
             const long long kx = (long long)(key >> bits_y);
             const long long ky = (long long)key & ymask;
             if (off.cheb1) {
-                // Chebyshev delta 1: (x+1,y+1) touches (x,y+1) and (x+1,y), and
-                // (x+1,y-1) touches (x+1,y); when those are significant their
-                // own forward probes make the diagonal edge redundant, so the
-                // diagonals are probed only when needed (fewer unsuccessful
-                // probes, the long ones).
-                nb[0] = sig_index(t, kx, ky, 0, 1, bits_y, xlim, ylim);
-                nb[2] = sig_index(t, kx, ky, 1, 0, bits_y, xlim, ylim);
+                sig_index2(t, kx, ky, make_int2(0, 1), make_int2(1, 0), bits_y, xlim, ylim, nb[0],
+                           nb[2]);
                 if (nb[2] == 0xffffffffu) {
-                    nb[1] = sig_index(t, kx, ky, 1, -1, bits_y, xlim, ylim);
-                    if (nb[0] == 0xffffffffu) nb[3] = sig_index(t, kx, ky, 1, 1, bits_y, xlim, ylim);
+                    if (nb[0] == 0xffffffffu)
+                        sig_index2(t, kx, ky, make_int2(1, -1), make_int2(1, 1), bits_y, xlim,
+                                   ylim, nb[1], nb[3]);
+                    else
+                        nb[1] = sig_index(t, kx, ky, 1, -1, bits_y, xlim, ylim);
                 }
             } else {
                 for (int o = 0; o < off.n; ++o) {
@@ -171,38 +193,34 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
                     if (o < kStoredNb)
                         nb[o] = j;
                     else
-                        uf_unite(parent, (u32)i, j);  // wide neighbourhoods (delta > 1)
+                        uf_unite(parent, (u32)i, j);
                 }
             }
         }
-        window_sync();
-        // window-local edges
+        __syncwarp();
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (nb[o] != 0xffffffffu && nb[o] >= base && nb[o] < base + kUnionWindow)
-                lunite(lp, loc, nb[o] - (u32)base);
-        window_sync();
-        const u32 r = lfind(lp, loc);
-        if (valid && r != loc) {
+            if (nb[o] != 0xffffffffu && nb[o] >= base && nb[o] < base + 32)
+                lunite(lp, (u32)lane, nb[o] - (u32)base);
+        __syncwarp();
+        const u32 r = lfind(lp, (u32)lane);
+        if (valid && r != (u32)lane) {
             const u32 target = (u32)base + r;  // < i: keeps parent[x] <= x
-            if (atomicCAS(parent + i, (u32)i, target) != (u32)i) uf_unite(parent, (u32)i, target);
+            if (!wide)
+                parent[i] = target;
+            else if (atomicCAS(parent + i, (u32)i, target) != (u32)i)
+                uf_unite(parent, (u32)i, target);
         }
-        // Edges leaving the window are deferred to k_union_edges, which runs
-        // once every window has linked its tiles to their local roots (finds
-        // are then short, and the divergent per-lane union loops become one
-        // uniform thread per edge). Edges are recorded from the local root;
-        // the block reserves its list space with one atomic. If the list is
-        // full the edge is united here.
+        // edges leaving the warp -> this window's fixed slots
         u32 ext = 0;
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + kUnionWindow)) {
+            if (nb[o] != 0xffffffffu && (nb[o] < base || nb[o] >= base + 32)) {
                 bool dup = false;
 #pragma unroll
                 for (int q = 0; q < o; ++q) dup |= nb[q] == nb[o];
                 if (!dup) ext |= 1u << o;
             }
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         const u32 cnt = __popc(ext);
         u32 incl = cnt;
 #pragma unroll
@@ -210,39 +228,27 @@ __global__ void __launch_bounds__(256) k_union(const u64* sig_key, const u64* n_
             const u32 y = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += y;
         }
-        if (lane == 31) s_wsum[wid] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            u32 tot = 0;
-            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-                const u32 c = s_wsum[q];
-                s_wsum[q] = tot;
-                tot += c;
-            }
-            s_base = tot ? atomicAdd(el.n, (u64)tot) : 0;
-        }
-        __syncthreads();
-        u64 at = s_base + s_wsum[wid] + incl - cnt;
+        uint2* slots = el.e + win * kEdgeSlots;
+        u32 at = incl - cnt;
 #pragma unroll
         for (int o = 0; o < kStoredNb; ++o)
-            if (ext >> o & 1) {
-                if (at < el.cap)
-                    el.e[at] = make_uint2((u32)base + r, nb[o]);
-                else
-                    uf_unite(parent, (u32)i, nb[o]);
-                ++at;
-            }
-        __syncthreads();
+            if (ext >> o & 1) slots[at++] = make_uint2((u32)base + r, nb[o]);
+        if (lane == 31) el.n[win] = incl;
+        __syncwarp();
     }
 }
 
-// Deferred window-external edges: one thread per edge.
-__global__ void k_union_edges(const uint2* e, const u64* n_p, u64 cap, u32* parent) {
-    const u64 n = min(*n_p, cap);
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x) {
-        const uint2 v = e[i];
-        uf_unite(parent, v.x, v.y);
+// Window-external edges: one warp per window, one lane per edge.
+__global__ void k_union_edges(EdgeList el, const u64* n_sig_p, u32* parent) {
+    const u64 n_win = (*n_sig_p + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    for (u64 w = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; w < n_win;
+         w += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32 n = el.n[w];
+        for (u32 j = lane; j < n; j += 32) {
+            const uint2 v = el.e[w * kEdgeSlots + j];
+            uf_unite(parent, v.x, v.y);
+        }
     }
 }
 
@@ -394,10 +400,9 @@ static int grid_for(u64 n, int n_sm, int per_sm = 8) {
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st) {
     const int gs = grid_for(A.n_sig, A.n_sm, 16);
     Offsets off{A.offsets, A.n_offsets, A.cheb1};
-    const EdgeList el{A.edges, A.edge_cap, &A.ctr->n_edges};
-    cudaMemsetAsync(&A.ctr->n_edges, 0, sizeof(u64), st);
+    const EdgeList el{A.edges, A.edge_n};
     k_union<<<gs, 256, 0, st>>>(A.sig_key, A.n_sig_dev, A.t, A.bits_y, A.bits_x, off, A.parent, el);
-    k_union_edges<<<gs, 256, 0, st>>>(A.edges, &A.ctr->n_edges, A.edge_cap, A.parent);
+    k_union_edges<<<gs, 256, 0, st>>>(el, A.n_sig_dev, A.parent);
     k_compress_reduce<<<gs, 256, 0, st>>>(A.parent, A.sig_key, A.sig_cnt, A.n_sig_dev, A.size,
                                           A.npts, A.min_key);
     k_select_roots<<<gs, 256, 0, st>>>(A.parent, A.size, A.min_key, A.n_sig_dev, A.mu,

@@ -166,8 +166,8 @@ struct rg_ctx {
     int *tile_cid = nullptr, *root_cid = nullptr;
     u64 *root_key = nullptr, *root_key_sorted = nullptr;
     u32 *root_idx = nullptr, *root_idx_sorted = nullptr;
-    uint2* edges = nullptr;  // K3 deferred edges, capacity edge_cap
-    u64 edge_cap = 0;
+    uint2* edges = nullptr;  // K3 deferred edges: 128 slots per 32-tile window
+    u32* edge_n = nullptr;   // edges per window
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -625,8 +625,8 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     dfree(ctx->root_idx);
     dfree(ctx->root_idx_sorted);
     dfree(ctx->edges);
+    dfree(ctx->edge_n);
     ctx->sig_cap = 0;
-    ctx->edge_cap = 0;
     const u64 c = std::max<u64>(n, 1024);
     CK(dalloc(&ctx->sig_key, c));
     CK(dalloc(&ctx->sig_cnt, c));
@@ -640,8 +640,8 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     CK(dalloc(&ctx->root_key_sorted, c));
     CK(dalloc(&ctx->root_idx, c));
     CK(dalloc(&ctx->root_idx_sorted, c));
-    CK(dalloc(&ctx->edges, c));  // overflow edges are united in place
-    ctx->edge_cap = c;
+    CK(dalloc(&ctx->edges, (c + 31) / 32 * 128));
+    CK(dalloc(&ctx->edge_n, (c + 31) / 32));
     ctx->sig_cap = c;
     return RG_OK;
 }
@@ -725,7 +725,7 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
     A.root_key_sorted = ctx->root_key_sorted;
     A.root_idx_sorted = ctx->root_idx_sorted;
     A.edges = ctx->edges;
-    A.edge_cap = ctx->edge_cap;
+    A.edge_n = ctx->edge_n;
     A.ctr = ctx->ctr;
     A.n_sm = ctx->n_sm;
     zero_field(ctx, &ctx->ctr->n_roots);
@@ -941,6 +941,7 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->root_idx);
     dfree(ctx->root_idx_sorted);
     dfree(ctx->edges);
+    dfree(ctx->edge_n);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {

@@ -52,8 +52,8 @@ struct AggLaunch {
     u64* min_key;
     int* root_cid;
     int* tile_cid;
-    uint2* edges;     // deferred external edges of k_union
-    u64 edge_cap;
+    uint2* edges;     // deferred external edges of k_union: 128 slots per 32-tile window
+    u32* edge_n;      // edges per window
     u64* root_key;
     u32* root_idx;
     u64* root_key_sorted;
