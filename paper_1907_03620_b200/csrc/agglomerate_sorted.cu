@@ -1,0 +1,323 @@
+// agglomerate_sorted.cu — K3 over the significant tiles in key order.
+//
+// Same contract as agglomerate.cu (connected_components agglomerate.hpp:124-170,
+// the mu filter :198-199 and finalize_clusters :175-191) but the tiles are
+// first radix-sorted by packed key, i.e. lexicographically by (tx, ty) — the
+// canonical order of finalize_clusters. Then:
+//   * neighbour discovery needs no hash probes: (x, y+1..y+r) are the next
+//     entries of the same column, and column x+dx's window [y-r, y+r] is found
+//     by a galloping search from the tile's own position (all L1/L2 hits:
+//     neighbours in key order are close in memory);
+//   * most edges join tiles a few positions apart, so a block resolves the
+//     edges among its 256 consecutive tiles in a shared-memory union-find and
+//     defers only the few edges leaving the window;
+//   * the root of a component (smallest index) is its smallest tile, so
+//     canonical cluster ids are an exclusive scan of "root with size >= mu"
+//     flags — no per-root minimum and no sort of the roots;
+//   * the sorted keys are the canonical output order.
+// Used for delta <= 2 (at most 12 forward offsets, bounded edge list).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rg {
+
+namespace {
+
+__device__ __forceinline__ u32 s_ld_parent(const u32* p) {
+    u32 v;
+    asm volatile("ld.global.relaxed.gpu.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ u32 s_find(u32* parent, u32 v) {
+    u32 par = s_ld_parent(parent + v);
+    if (par != v) {
+        u32 prev = v, next;
+        while (par > (next = s_ld_parent(parent + par))) {
+            parent[prev] = next;
+            prev = par;
+            par = next;
+        }
+    }
+    return par;
+}
+
+__device__ __forceinline__ void s_unite(u32* parent, u32 a, u32 b) {
+    u32 ra = s_find(parent, a), rb = s_find(parent, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 t = ra;
+            ra = rb;
+            rb = t;
+        }
+        const u32 old = atomicCAS(parent + ra, ra, rb);
+        if (old == ra) return;
+        ra = old;
+    }
+}
+
+__device__ __forceinline__ u32 l_find(volatile u32* lp, u32 x) {
+    u32 p;
+    while ((p = lp[x]) != x) x = p;
+    return x;
+}
+
+__device__ __forceinline__ void l_unite(u32* lp, u32 a, u32 b) {
+    volatile u32* v = lp;
+    u32 ra = l_find(v, a), rb = l_find(v, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 t = ra;
+            ra = rb;
+            rb = t;
+        }
+        const u32 old = atomicCAS(lp + ra, ra, rb);
+        if (old == ra) return;
+        ra = l_find(v, old);
+        rb = l_find(v, rb);
+    }
+}
+
+// First index j >= from with key[j] >= target (galloping, then binary).
+__device__ __forceinline__ u64 gallop(const u64* key, u64 n, u64 from, u64 target) {
+    if (from >= n || key[from] >= target) return from;
+    u64 lo = from, step = 1, hi = from + 1;
+    while (hi < n && key[hi] < target) {
+        lo = hi;
+        step <<= 1;
+        hi = from + step;
+    }
+    if (hi > n) hi = n;
+    // key[lo] < target; answer in (lo, hi]
+    u64 a = lo + 1, b = hi;
+    while (a < b) {
+        const u64 m = (a + b) >> 1;
+        if (key[m] < target)
+            a = m + 1;
+        else
+            b = m;
+    }
+    return a;
+}
+
+}  // namespace
+
+struct SortedEdges {
+    uint2* e;
+    u64 cap;
+    u64* n;
+};
+
+// Window = the 256 consecutive tiles of a block.
+__global__ void __launch_bounds__(256) k_sorted_union(const u64* skey, const u64* n_sig_p,
+                                                      u32 bits_y, int delta, int manhattan,
+                                                      u32* parent, u32* size, u64* npts,
+                                                      SortedEdges el) {
+    __shared__ u32 s_par[256];
+    __shared__ u32 s_wcnt[8];
+    __shared__ u64 s_base;
+    const u64 n = *n_sig_p;
+    const u32 loc = threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 ymask = (1ull << bits_y) - 1;
+    const u64 span = (n + 255) / 256 * 256;
+    for (u64 i = blockIdx.x * 256ull + loc; i < span; i += (u64)gridDim.x * 256) {
+        const u64 base = i - loc;
+        const u64 wend = base + 256;
+        const bool valid = i < n;
+        s_par[loc] = loc;
+        __syncthreads();
+        u32 ext[12];
+        int n_ext = 0;
+        if (valid) {
+            const u64 k = skey[i];
+            const u64 x = k >> bits_y, y = k & ymask;
+            // same column, rows y+1 .. y+delta: the next entries
+            for (u64 j = i + 1; j < n; ++j) {
+                const u64 kj = skey[j];
+                if ((kj >> bits_y) != x || (kj & ymask) > y + (u64)delta) break;
+                if (j < wend)
+                    l_unite(s_par, loc, (u32)(j - base));
+                else if (n_ext < 12)
+                    ext[n_ext++] = (u32)j;
+            }
+            // columns x+1 .. x+delta
+            u64 from = i + 1;
+            for (int dx = 1; dx <= delta; ++dx) {
+                const u64 r = manhattan ? (u64)(delta - dx) : (u64)delta;
+                const u64 nx = x + (u64)dx;
+                if (nx >> (63 - bits_y)) break;  // beyond the key space
+                const u64 ylo = y >= r ? y - r : 0;
+                const u64 lo_key = (nx << bits_y) | ylo;
+                const u64 hi_key = (nx << bits_y) | min(y + r, ymask);
+                u64 j = gallop(skey, n, from, lo_key);
+                from = j;
+                for (; j < n && skey[j] <= hi_key; ++j) {
+                    if (j < wend)
+                        l_unite(s_par, loc, (u32)(j - base));
+                    else if (n_ext < 12)
+                        ext[n_ext++] = (u32)j;
+                }
+            }
+        }
+        __syncthreads();
+        const u32 r = l_find(s_par, loc);
+        if (valid) {
+            parent[i] = (u32)base + r;  // <= i; sole writer of parent[i] in this kernel
+            size[i] = 0;
+            npts[i] = 0;
+        }
+        // deferred window-external edges: block-aggregated reservation
+        u32 incl = (u32)n_ext;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 yv = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += yv;
+        }
+        if (lane == 31) s_wcnt[wid] = incl;
+        __syncthreads();
+        if (loc == 0) {
+            u32 tot = 0;
+            for (int q = 0; q < 8; ++q) {
+                const u32 c = s_wcnt[q];
+                s_wcnt[q] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(el.n, (u64)tot) : 0;
+        }
+        __syncthreads();
+        u64 at = s_base + s_wcnt[wid] + incl - (u32)n_ext;
+        for (int q = 0; q < n_ext; ++q, ++at)
+            if (at < el.cap) el.e[at] = make_uint2((u32)base + r, ext[q]);
+        __syncthreads();
+    }
+}
+
+__global__ void k_sorted_edges(SortedEdges el, u32* parent) {
+    const u64 n = min(*el.n, el.cap);
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const uint2 v = el.e[i];
+        s_unite(parent, v.x, v.y);
+    }
+}
+
+// Flatten + per-root tile and point counts (segmented warp reduction over
+// runs of equal roots; only run heads touch global memory). Counts are read
+// through the sort permutation.
+__global__ void k_sorted_reduce(u32* parent, const u32* perm, const u64* cnt_b,
+                                const u64* n_sig_p, u32* size, u64* npts, u32* is_root,
+                                u64 mu) {
+    const u64 n = *n_sig_p;
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const bool valid = i < n;
+        u32 r = 0xffffffffu;
+        if (valid) {
+            const u32 old = s_ld_parent(parent + i);
+            u32 next;
+            r = old;
+            while (r > (next = s_ld_parent(parent + r))) r = next;
+            if (r != old) parent[i] = r;
+        }
+        u32 c = valid ? 1u : 0u;
+        u64 p = valid && cnt_b ? cnt_b[perm[i]] : 0ull;
+        const u32 prev = __shfl_up_sync(kFull, r, 1);
+        const bool head = lane == 0 || prev != r;
+        const u32 heads = __ballot_sync(kFull, head);
+        const u32 run = __popc(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 orun = __shfl_down_sync(kFull, run, o);
+            const u32 oc = __shfl_down_sync(kFull, c, o);
+            const u64 op = __shfl_down_sync(kFull, p, o);
+            if (lane + o < 32 && orun == run) {
+                c += oc;
+                p += op;
+            }
+        }
+        if (head && valid) {
+            atomicAdd(size + r, c);
+            atomicAdd(npts + r, p);
+        }
+    }
+}
+
+// Kept-root flags (input of the id scan), after every size is final.
+__global__ void k_sorted_flags(const u32* parent, const u32* size, const u64* n_sig_p, u64 mu,
+                               u32* flag, Counters* ctr) {
+    const u64 n = *n_sig_p;
+    u32 roots = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const bool root = parent[i] == (u32)i;
+        roots += root;
+        flag[i] = (root && size[i] >= mu) ? 1u : 0u;
+    }
+    const u32 w = __reduce_add_sync(kFull, roots);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&ctr->n_roots, (u64)w);
+}
+
+// Canonical ids: id of a tile = scan value at its root; scattered to bucket
+// order for the labelling pass; cluster k's root recorded for cluster facts.
+__global__ void k_sorted_label(const u32* parent, const u32* flag, const u32* scan,
+                               const u32* perm, const u64* n_sig_p, int* tile_cid_b,
+                               int* cid_s, u32* clu_root, Counters* ctr) {
+    const u64 n = *n_sig_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 r = parent[i];
+        const int cid = flag[r] ? (int)scan[r] : -1;
+        cid_s[i] = cid;
+        tile_cid_b[perm[i]] = cid;
+        if (r == (u32)i && cid >= 0) clu_root[cid] = (u32)i;
+        if (i == n - 1) ctr->n_kept = (u64)scan[i] + flag[i];
+    }
+}
+
+static int grid_for_s(u64 n, int n_sm, int per_sm) {
+    const u64 want = (n + 255) / 256;
+    const u64 cap = (u64)n_sm * per_sm;
+    return (int)(want == 0 ? 1 : (want < cap ? want : cap));
+}
+
+size_t sorted_temp_bytes(u64 n, int bits) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs((void*)nullptr, a, (const u64*)nullptr, (u64*)nullptr,
+                                    (const u32*)nullptr, (u32*)nullptr, (int)n, 0, bits);
+    cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const u32*)nullptr, (u32*)nullptr, (int)n);
+    return a > b ? a : b;
+}
+
+cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
+    const u64 n = L.n_sig;
+    if (n == 0) return cudaSuccess;
+    const int gs = grid_for_s(n, L.n_sm, 16);
+    cudaError_t e = launch_iota(L.iota, n, L.n_sm, st);
+    if (e != cudaSuccess) return e;
+    size_t bytes = L.temp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(L.temp, bytes, L.sig_key, L.skey, L.iota, L.perm, (int)n,
+                                        0, (int)L.key_bits, st);
+    if (e != cudaSuccess) return e;
+    SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
+    cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
+    k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta, L.manhattan,
+                                       L.parent, L.size, L.npts, el);
+    k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
+    k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size, L.npts,
+                                        L.flag, L.mu);
+    k_sorted_flags<<<gs, 256, 0, st>>>(L.parent, L.size, L.n_sig_dev, L.mu, L.flag, L.ctr);
+    bytes = L.temp_bytes;
+    e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.flag, L.scan, (int)n, st);
+    if (e != cudaSuccess) return e;
+    k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.flag, L.scan, L.perm, L.n_sig_dev,
+                                       L.tile_cid_b, L.cid_s, L.clu_root, L.ctr);
+    return cudaGetLastError();
+}
+
+}  // namespace rg

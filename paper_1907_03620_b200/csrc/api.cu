@@ -93,14 +93,17 @@ __global__ void k_gather_sorted(const u32* order, const u64* key, const u64* cnt
     }
 }
 
-__global__ void k_cluster_facts(const u64* root_key_sorted, const u32* root_idx_sorted, u64 n,
-                                const u32* size, const u64* npts, Grid res, u64* n_tiles,
-                                u64* n_points, long long* fx, long long* fy) {
+__global__ void k_cluster_facts(const u64* root_key_sorted, const u32* root_idx_sorted,
+                                const u32* clu_root, u64 n, const u32* size, const u64* npts,
+                                Grid res, u64* n_tiles, u64* n_points, long long* fx,
+                                long long* fy) {
     const u64 ymask = (1ull << res.bits_y) - 1;
     for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < n;
          k += (u64)gridDim.x * blockDim.x) {
-        const u32 r = root_idx_sorted[k];
-        const u64 key = root_key_sorted[k];
+        // hash path: k-th kept root and its smallest key; sorted path: the
+        // root's sorted position, whose key is the smallest of its cluster
+        const u32 r = clu_root ? clu_root[k] : root_idx_sorted[k];
+        const u64 key = root_key_sorted[clu_root ? r : k];
         if (n_tiles) n_tiles[k] = size[r];
         if (n_points) n_points[k] = npts[r];
         if (fx) fx[k] = res.origin_x + (long long)(key >> res.bits_y);
@@ -168,6 +171,12 @@ struct rg_ctx {
     u32 *root_idx = nullptr, *root_idx_sorted = nullptr;
     uint2* edges = nullptr;  // K3 deferred edges: 128 slots per 32-tile window
     u32* edge_n = nullptr;   // edges per window
+    // key-sorted K3 (agglomerate_sorted.cu)
+    bool sorted = false;     // current result came from the sorted path
+    u32 *s_flag = nullptr, *s_scan = nullptr, *s_clu_root = nullptr;
+    int* s_cid = nullptr;
+    uint2* s_edges = nullptr;
+    u64 s_cap = 0, s_edge_cap = 0;
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -656,6 +665,12 @@ rg_status ensure_sort_temp(rg_ctx* ctx, u64 n, int bits) {
     return RG_OK;
 }
 
+bool use_sorted_k3(const rg_ctx* ctx) {
+    static const char* force = std::getenv("RG_K3");  // "hash" forces the hash-probe path
+    if (force && std::strcmp(force, "hash") == 0) return false;
+    return ctx->p.distance <= 2 && ctx->used < 0x7fffffffull;  // S <= D = used
+}
+
 rg_status prune_impl(rg_ctx* ctx) {
     if (ctx->state != rg_ctx::kAccum) {
         // prune() on a consumed accumulator returns nothing (empty table).
@@ -667,9 +682,10 @@ rg_status prune_impl(rg_ctx* ctx) {
     PhaseTimer timer(ctx, &ctx->ms_prune);
     zero_field(ctx, &ctx->ctr->n_sig);
     if (ctx->slots && ctx->used) {
+        const bool hash_k3 = !use_sorted_k3(ctx);
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
-                          ctx->parent, ctx->size, ctx->npts, ctx->min_key, ctx->root_cid, ctx->ctr,
-                          ctx->n_sm, ctx->st));
+                          ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
+                          ctx->root_cid, ctx->ctr, ctx->n_sm, ctx->st));
         ++ctx->launches;
     }
     CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, sizeof(u64), cudaMemcpyDeviceToHost,
@@ -678,10 +694,82 @@ rg_status prune_impl(rg_ctx* ctx) {
     timer.stop();
     ctx->n_sig = ctx->hctr->n_sig;
     ctx->state = rg_ctx::kSig;
+    ctx->sorted = false;
     ctx->table_dirty = true;
     ctx->res = ctx->grid;
     ctx->res_is_canvas = true;
     ctx->n_roots = ctx->n_kept = 0;
+    return RG_OK;
+}
+
+
+rg_status agglomerate_sorted_impl(rg_ctx* ctx) {
+    const u64 n = ctx->n_sig;
+    const int kb = (int)(ctx->res.bits_x + ctx->res.bits_y);
+    if (ctx->s_cap < n || !ctx->s_flag) {
+        dfree(ctx->s_flag);
+        dfree(ctx->s_scan);
+        dfree(ctx->s_clu_root);
+        dfree(ctx->s_cid);
+        ctx->s_cap = 0;
+        const u64 c = std::max<u64>(n, 1024);
+        CK(dalloc(&ctx->s_flag, c));
+        CK(dalloc(&ctx->s_scan, c));
+        CK(dalloc(&ctx->s_clu_root, c));
+        CK(dalloc(&ctx->s_cid, c));
+        ctx->s_cap = c;
+    }
+    const u64 ecap = std::max<u64>(n, 1024) * (u64)std::min(ctx->n_offsets, 12);
+    if (ctx->s_edge_cap < ecap) {
+        dfree(ctx->s_edges);
+        ctx->s_edge_cap = 0;
+        CK(dalloc(&ctx->s_edges, ecap));
+        ctx->s_edge_cap = ecap;
+    }
+    const size_t tb = sorted_temp_bytes(n, kb);
+    if (ctx->sort_temp_bytes < tb || !ctx->sort_temp) {
+        dfree(ctx->sort_temp);
+        ctx->sort_temp_bytes = 0;
+        CK(cudaMalloc(&ctx->sort_temp, tb));
+        ctx->sort_temp_bytes = tb;
+    }
+    SortedLaunch L;
+    L.sig_key = ctx->sig_key;
+    L.sig_cnt = ctx->sig_cnt;
+    L.n_sig_dev = &ctx->ctr->n_sig;
+    L.n_sig = n;
+    L.bits_y = ctx->res.bits_y;
+    L.key_bits = (u32)kb;
+    L.delta = ctx->p.distance;
+    L.manhattan = ctx->p.metric == RG_METRIC_MANHATTAN;
+    L.mu = ctx->p.min_cluster_size;
+    L.iota = ctx->root_idx;
+    L.skey = ctx->root_key_sorted;
+    L.perm = ctx->root_idx_sorted;
+    L.parent = ctx->parent;
+    L.size = ctx->size;
+    L.npts = ctx->npts;
+    L.flag = ctx->s_flag;
+    L.scan = ctx->s_scan;
+    L.tile_cid_b = ctx->tile_cid;
+    L.cid_s = ctx->s_cid;
+    L.clu_root = ctx->s_clu_root;
+    L.edges = ctx->s_edges;
+    L.edge_cap = ctx->s_edge_cap;
+    L.temp = ctx->sort_temp;
+    L.temp_bytes = ctx->sort_temp_bytes;
+    L.ctr = ctx->ctr;
+    L.n_sm = ctx->n_sm;
+    zero_field(ctx, &ctx->ctr->n_roots);
+    zero_field(ctx, &ctx->ctr->n_kept);
+    CK(launch_agglomerate_sorted(L, ctx->st));
+    ctx->launches += 14;  // iota + radix sort (6) + union, edges, reduce, flags, scan (2), label
+    CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
+                       cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->n_roots = ctx->hctr->n_roots;
+    ctx->n_kept = ctx->hctr->n_kept;
+    ctx->sorted = true;
     return RG_OK;
 }
 
@@ -690,7 +778,15 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
         return set_err(ctx, RG_ERR_STATE, "agglomerate requires a pruned or loaded tile set");
     PhaseTimer timer(ctx, &ctx->ms_agg);
     ctx->n_roots = ctx->n_kept = 0;
+    ctx->sorted = false;
     if (ctx->n_sig == 0) {
+        ctx->state = rg_ctx::kAgg;
+        return RG_OK;
+    }
+    if (use_sorted_k3(ctx)) {
+        rg_status s = agglomerate_sorted_impl(ctx);
+        if (s != RG_OK) return s;
+        timer.stop();
         ctx->state = rg_ctx::kAgg;
         return RG_OK;
     }
@@ -942,6 +1038,11 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->root_idx_sorted);
     dfree(ctx->edges);
     dfree(ctx->edge_n);
+    dfree(ctx->s_flag);
+    dfree(ctx->s_scan);
+    dfree(ctx->s_clu_root);
+    dfree(ctx->s_cid);
+    dfree(ctx->s_edges);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {
@@ -1198,6 +1299,7 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     ctx->res = res;
     ctx->res_is_canvas = on_canvas;
     ctx->state = rg_ctx::kSig;
+    ctx->sorted = false;
     ctx->table_dirty = true;
     return RG_OK;
 }
@@ -1267,15 +1369,19 @@ rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* co
     const int bits = (int)(ctx->res.bits_x + ctx->res.bits_y);
     u64* ks = nullptr;
     u32 *iota = nullptr, *order = nullptr;
-    CK(dalloc(&ks, n));
-    CK(dalloc(&iota, n));
-    CK(dalloc(&order, n));
     void* temp = nullptr;
-    const size_t tb = sort_pairs_temp_bytes(n, bits);
-    CK(cudaMalloc(&temp, tb));
-    CK(launch_iota(iota, n, ctx->n_sm, ctx->st));
-    CK(sort_pairs(temp, tb, ctx->sig_key, ks, iota, order, n, bits, ctx->st));
-    ctx->launches += 6;
+    if (ctx->state == rg_ctx::kAgg && ctx->sorted) {
+        order = ctx->root_idx_sorted;  // K3 already sorted the keys
+    } else {
+        CK(dalloc(&ks, n));
+        CK(dalloc(&iota, n));
+        CK(dalloc(&order, n));
+        const size_t tb = sort_pairs_temp_bytes(n, bits);
+        CK(cudaMalloc(&temp, tb));
+        CK(launch_iota(iota, n, ctx->n_sm, ctx->st));
+        CK(sort_pairs(temp, tb, ctx->sig_key, ks, iota, order, n, bits, ctx->st));
+        ctx->launches += 6;
+    }
     long long *dtx = (long long*)tx, *dty = (long long*)ty, *dcid = (long long*)cluster_id;
     u64* dcnt = (u64*)count;
     if (kind == RG_MEM_HOST) {
@@ -1303,10 +1409,10 @@ rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* co
         dfree(dcnt);
         dfree(dcid);
     }
-    cudaFree(temp);
+    if (temp) cudaFree(temp);
     dfree(ks);
     dfree(iota);
-    dfree(order);
+    if (!(ctx->state == rg_ctx::kAgg && ctx->sorted)) dfree(order);
     return RG_OK;
 }
 
@@ -1329,8 +1435,8 @@ rg_status rg_get_clusters(rg_ctx* ctx, uint64_t* n_tiles, uint64_t* n_points, in
         if (first_ty) CK(dalloc(&dfy, w));
     }
     k_cluster_facts<<<grid_for(w, ctx->n_sm), 256, 0, ctx->st>>>(
-        ctx->root_key_sorted, ctx->root_idx_sorted, w, ctx->size, ctx->npts, ctx->res, dnt, dnp,
-        dfx, dfy);
+        ctx->root_key_sorted, ctx->root_idx_sorted, ctx->sorted ? ctx->s_clu_root : nullptr, w,
+        ctx->size, ctx->npts, ctx->res, dnt, dnp, dfx, dfy);
     ++ctx->launches;
     CK(cudaGetLastError());
     if (kind == RG_MEM_HOST) {

@@ -463,10 +463,12 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
         o.sig_key[pos] = k;
         o.sig_cnt[pos] = v;
         o.parent[pos] = (u32)pos;
-        o.size[pos] = 0;
-        o.npts[pos] = 0;
-        o.min_key[pos] = kEmpty;
-        o.root_cid[pos] = -1;
+        if (o.size) {  // hash-probe K3 only (the sorted K3 initialises its own)
+            o.size[pos] = 0;
+            o.npts[pos] = 0;
+            o.min_key[pos] = kEmpty;
+            o.root_cid[pos] = -1;
+        }
         t.slots[i].count = kSigBit | pos;
     }
     __syncwarp();

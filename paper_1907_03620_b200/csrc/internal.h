@@ -65,6 +65,36 @@ struct AggLaunch {
 };
 
 cudaError_t launch_agglomerate(const AggLaunch& A, cudaStream_t st);
+
+// K3 over key-sorted tiles (agglomerate_sorted.cu), delta <= 2.
+struct SortedLaunch {
+    const u64* sig_key;   // bucket order (K2 output)
+    const u64* sig_cnt;
+    const u64* n_sig_dev;
+    u64 n_sig;
+    u32 bits_y, key_bits;
+    int delta, manhattan;
+    u64 mu;
+    u32* iota;            // scratch, S
+    u64* skey;            // sorted keys, S
+    u32* perm;            // sorted position -> bucket index, S
+    u32* parent;          // sorted space
+    u32* size;
+    u64* npts;
+    u32* flag;
+    u32* scan;
+    int* tile_cid_b;      // cluster id per bucket index (labelling pass)
+    int* cid_s;           // cluster id per sorted position (canonical output)
+    u32* clu_root;        // sorted position of cluster k's root
+    uint2* edges;
+    u64 edge_cap;
+    void* temp;
+    size_t temp_bytes;
+    Counters* ctr;
+    int n_sm;
+};
+size_t sorted_temp_bytes(u64 n, int bits);
+cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st);
 cudaError_t launch_order_and_label(const AggLaunch& A, u64 n_kept, cudaStream_t st);
 size_t sort_pairs_temp_bytes(u64 n, int bits);
 cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_out,
