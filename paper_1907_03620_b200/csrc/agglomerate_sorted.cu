@@ -18,6 +18,7 @@
 // Used for delta <= 2 (at most 12 forward offsets, bounded edge list).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -280,30 +281,83 @@ __global__ void k_sorted_label(const u32* parent, const u32* flag, const u32* sc
     }
 }
 
+// Key sort by columns (when the column field has <= kColBitsMax bits): a
+// counting sort on the column (histogram, scan, scatter), then a segmented
+// sort of each column by row — two passes over the data instead of the
+// radix sort's five, and columns are short (tens of tiles).
+constexpr u32 kColBitsMax = 22;
+
+__global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt) {
+    const u64 n = *n_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        atomicAdd(cnt + (key[i] >> bits_y), 1u);
+}
+
+__global__ void k_col_scatter(const u64* key, const u64* n_p, u32 bits_y, u32* cursor,
+                              u64* k_out, u32* v_out) {
+    const u64 n = *n_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 k = key[i];
+        const u32 at = atomicAdd(cursor + (k >> bits_y), 1u);
+        k_out[at] = k;
+        v_out[at] = (u32)i;
+    }
+}
+
 static int grid_for_s(u64 n, int n_sm, int per_sm) {
     const u64 want = (n + 255) / 256;
     const u64 cap = (u64)n_sm * per_sm;
     return (int)(want == 0 ? 1 : (want < cap ? want : cap));
 }
 
-size_t sorted_temp_bytes(u64 n, int bits) {
-    size_t a = 0, b = 0;
+u64 sorted_columns(u32 bits_x) { return bits_x <= kColBitsMax ? (1ull << bits_x) : 0; }
+
+size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x) {
+    size_t a = 0, b = 0, c = 0, d = 0;
     cub::DeviceRadixSort::SortPairs((void*)nullptr, a, (const u64*)nullptr, (u64*)nullptr,
                                     (const u32*)nullptr, (u32*)nullptr, (int)n, 0, bits);
     cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const u32*)nullptr, (u32*)nullptr, (int)n);
-    return a > b ? a : b;
+    const u64 cols = sorted_columns(bits_x);
+    if (cols) {
+        cub::DeviceScan::ExclusiveSum((void*)nullptr, c, (const u32*)nullptr, (u32*)nullptr,
+                                      (int)(cols + 1));
+        cub::DeviceSegmentedSort::SortPairs((void*)nullptr, d, (const u64*)nullptr,
+                                            (u64*)nullptr, (const u32*)nullptr, (u32*)nullptr,
+                                            (int)n, (int)cols, (const u32*)nullptr,
+                                            (const u32*)nullptr);
+    }
+    return std::max(std::max(a, b), std::max(c, d));
 }
 
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     const u64 n = L.n_sig;
     if (n == 0) return cudaSuccess;
     const int gs = grid_for_s(n, L.n_sm, 16);
-    cudaError_t e = launch_iota(L.iota, n, L.n_sm, st);
-    if (e != cudaSuccess) return e;
+    cudaError_t e;
     size_t bytes = L.temp_bytes;
-    e = cub::DeviceRadixSort::SortPairs(L.temp, bytes, L.sig_key, L.skey, L.iota, L.perm, (int)n,
-                                        0, (int)L.key_bits, st);
-    if (e != cudaSuccess) return e;
+    const u64 cols = sorted_columns(L.key_bits - L.bits_y);
+    if (cols && L.col_cnt) {
+        cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
+        k_col_hist<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt);
+        e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
+        if (e != cudaSuccess) return e;
+        cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
+                        st);
+        k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
+                                          L.iota);
+        bytes = L.temp_bytes;
+        e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
+                                                (int)n, (int)cols, L.col_off, L.col_off + 1, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        e = launch_iota(L.iota, n, L.n_sm, st);
+        if (e != cudaSuccess) return e;
+        e = cub::DeviceRadixSort::SortPairs(L.temp, bytes, L.sig_key, L.skey, L.iota, L.perm,
+                                            (int)n, 0, (int)L.key_bits, st);
+        if (e != cudaSuccess) return e;
+    }
     SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
     cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
     k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta, L.manhattan,

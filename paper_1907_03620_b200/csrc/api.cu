@@ -177,6 +177,8 @@ struct rg_ctx {
     int* s_cid = nullptr;
     uint2* s_edges = nullptr;
     u64 s_cap = 0, s_edge_cap = 0;
+    u32 *s_col_cnt = nullptr, *s_col_off = nullptr;
+    u64 s_cols = 0;
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -726,7 +728,16 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx) {
         CK(dalloc(&ctx->s_edges, ecap));
         ctx->s_edge_cap = ecap;
     }
-    const size_t tb = sorted_temp_bytes(n, kb);
+    const u64 cols = sorted_columns(ctx->res.bits_x);
+    if (cols && ctx->s_cols < cols) {
+        dfree(ctx->s_col_cnt);
+        dfree(ctx->s_col_off);
+        ctx->s_cols = 0;
+        CK(dalloc(&ctx->s_col_cnt, cols + 1));
+        CK(dalloc(&ctx->s_col_off, cols + 1));
+        ctx->s_cols = cols;
+    }
+    const size_t tb = sorted_temp_bytes(n, kb, ctx->res.bits_x);
     if (ctx->sort_temp_bytes < tb || !ctx->sort_temp) {
         dfree(ctx->sort_temp);
         ctx->sort_temp_bytes = 0;
@@ -744,6 +755,9 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx) {
     L.manhattan = ctx->p.metric == RG_METRIC_MANHATTAN;
     L.mu = ctx->p.min_cluster_size;
     L.iota = ctx->root_idx;
+    L.ktmp = ctx->root_key;
+    L.col_cnt = cols ? ctx->s_col_cnt : nullptr;
+    L.col_off = cols ? ctx->s_col_off : nullptr;
     L.skey = ctx->root_key_sorted;
     L.perm = ctx->root_idx_sorted;
     L.parent = ctx->parent;
@@ -1043,6 +1057,8 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->s_clu_root);
     dfree(ctx->s_cid);
     dfree(ctx->s_edges);
+    dfree(ctx->s_col_cnt);
+    dfree(ctx->s_col_off);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {

@@ -76,6 +76,9 @@ struct SortedLaunch {
     int delta, manhattan;
     u64 mu;
     u32* iota;            // scratch, S
+    u64* ktmp;            // scratch, S
+    u32* col_cnt;         // column counting sort: 2^bits_x + 1 entries (or null)
+    u32* col_off;
     u64* skey;            // sorted keys, S
     u32* perm;            // sorted position -> bucket index, S
     u32* parent;          // sorted space
@@ -93,7 +96,8 @@ struct SortedLaunch {
     Counters* ctr;
     int n_sm;
 };
-size_t sorted_temp_bytes(u64 n, int bits);
+size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
+u64 sorted_columns(u32 bits_x);
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st);
 cudaError_t launch_order_and_label(const AggLaunch& A, u64 n_kept, cudaStream_t st);
 size_t sort_pairs_temp_bytes(u64 n, int bits);
