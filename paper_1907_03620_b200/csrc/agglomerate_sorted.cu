@@ -197,6 +197,117 @@ __global__ void __launch_bounds__(256) k_sorted_union(const u64* skey, const u64
     }
 }
 
+// Chebyshev delta 1 (the BASELINE setting): at most four forward neighbours
+// (x, y+1) = the next entry, and (x+1, y-1..y+1) found by one galloping
+// search. A diagonal edge is dropped when an orthogonal neighbour makes it
+// redundant ((x+1,y+1) touches (x,y+1) and (x+1,y); (x+1,y-1) touches
+// (x+1,y)). Window-local components are found by min-label propagation with
+// pointer jumping in shared memory (converges in a few rounds; labels only
+// decrease), then every tile is linked to its component's smallest member.
+__global__ void __launch_bounds__(256) k_sorted_union_c1(const u64* skey, const u64* n_sig_p,
+                                                         u32 bits_y, u32* parent, u32* size,
+                                                         u64* npts, SortedEdges el) {
+    __shared__ u32 s_lbl[256];
+    __shared__ u32 s_wcnt[8];
+    __shared__ u64 s_base;
+    const u64 n = *n_sig_p;
+    const u32 loc = threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const u64 ymask = (1ull << bits_y) - 1;
+    const u64 span = (n + 255) / 256 * 256;
+    for (u64 i = blockIdx.x * 256ull + loc; i < span; i += (u64)gridDim.x * 256) {
+        const u64 base = i - loc;
+        const u64 wend = base + 256;
+        const bool valid = i < n;
+        u32 nb[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+        if (valid) {
+            const u64 k = skey[i];
+            const u64 y = k & ymask;
+            if (i + 1 < n && skey[i + 1] == k + 1) nb[0] = (u32)(i + 1);  // (x, y+1)
+            const u64 nxk = k + (1ull << bits_y);                          // (x+1, y)
+            if ((nxk >> bits_y) == (k >> bits_y) + 1) {
+                const u64 lo = y > 0 ? nxk - 1 : nxk;
+                u64 j = gallop(skey, n, i + 1, lo);
+                u32 dm = 0xffffffffu, d0 = 0xffffffffu, dp = 0xffffffffu;
+                for (; j < n && skey[j] <= nxk + 1 && (y < ymask || skey[j] <= nxk); ++j) {
+                    const u64 kj = skey[j];
+                    if (kj == nxk - 1 && y > 0) dm = (u32)j;
+                    else if (kj == nxk) d0 = (u32)j;
+                    else if (kj == nxk + 1) dp = (u32)j;
+                }
+                nb[2] = d0;
+                if (d0 == 0xffffffffu) {
+                    nb[1] = dm;
+                    if (nb[0] == 0xffffffffu) nb[3] = dp;
+                }
+            }
+        }
+        s_lbl[loc] = loc;
+        __syncthreads();
+        while (true) {
+            bool ch = false;
+            u32 m = s_lbl[loc];
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+                if (nb[o] < wend && nb[o] >= base) m = min(m, s_lbl[nb[o] - base]);
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+                if (nb[o] < wend && nb[o] >= base && s_lbl[nb[o] - base] > m) {
+                    atomicMin(&s_lbl[nb[o] - base], m);
+                    ch = true;
+                }
+            if (m < s_lbl[loc]) {
+                atomicMin(&s_lbl[loc], m);
+                ch = true;
+            }
+            __syncthreads();
+            const u32 l = s_lbl[loc];
+            const u32 ll = s_lbl[l];
+            if (ll < l) {
+                atomicMin(&s_lbl[loc], ll);
+                ch = true;
+            }
+            if (!__syncthreads_or(ch)) break;
+        }
+        const u32 r = s_lbl[loc];
+        if (valid) {
+            parent[i] = (u32)base + r;  // <= i; sole writer of parent[i] in this kernel
+            size[i] = 0;
+            npts[i] = 0;
+        }
+        // deferred window-external edges: block-aggregated reservation
+        u32 n_ext = 0;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) n_ext += (nb[o] != 0xffffffffu && nb[o] >= wend);
+        u32 incl = n_ext;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 yv = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += yv;
+        }
+        if (lane == 31) s_wcnt[wid] = incl;
+        __syncthreads();
+        if (loc == 0) {
+            u32 tot = 0;
+            for (int q = 0; q < 8; ++q) {
+                const u32 c = s_wcnt[q];
+                s_wcnt[q] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(el.n, (u64)tot) : 0;
+        }
+        __syncthreads();
+        u64 at = s_base + s_wcnt[wid] + incl - n_ext;
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+            if (nb[o] != 0xffffffffu && nb[o] >= wend) {
+                if (at < el.cap) el.e[at] = make_uint2((u32)base + r, nb[o]);
+                ++at;
+            }
+        __syncthreads();
+    }
+}
+
 __global__ void k_sorted_edges(SortedEdges el, u32* parent) {
     const u64 n = min(*el.n, el.cap);
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
@@ -360,8 +471,12 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     }
     SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
     cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
-    k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta, L.manhattan,
-                                       L.parent, L.size, L.npts, el);
+    if (L.delta == 1 && !L.manhattan)
+        k_sorted_union_c1<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.parent, L.size,
+                                              L.npts, el);
+    else
+        k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta, L.manhattan,
+                                           L.parent, L.size, L.npts, el);
     k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
     k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size, L.npts,
                                         L.flag, L.mu);
