@@ -398,22 +398,125 @@ __global__ void k_sorted_label(const u32* parent, const u32* flag, const u32* sc
 // radix sort's five, and columns are short (tens of tiles).
 constexpr u32 kColBitsMax = 22;
 
-__global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt) {
+__global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt, u32* max_col) {
+    // Consecutive tiles (bucket order) share columns: one atomic per column
+    // group of a warp.
     const u64 n = *n_p;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x)
-        atomicAdd(cnt + (key[i] >> bits_y), 1u);
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    u32 mx = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const bool valid = i < n;
+        const u32 col = valid ? (u32)(key[i] >> bits_y) : 0xffffffffu;
+        const u32 peers = __match_any_sync(kFull, col);
+        if (valid && lane == __ffs(peers) - 1) {
+            const u32 c = atomicAdd(cnt + col, (u32)__popc(peers)) + __popc(peers);
+            mx = max(mx, c);
+        }
+    }
+    mx = __reduce_max_sync(kFull, mx);
+    if (lane == 0 && mx) atomicMax(max_col, mx);
 }
 
 __global__ void k_col_scatter(const u64* key, const u64* n_p, u32 bits_y, u32* cursor,
                               u64* k_out, u32* v_out) {
     const u64 n = *n_p;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
          i += (u64)gridDim.x * blockDim.x) {
-        const u64 k = key[i];
-        const u32 at = atomicAdd(cursor + (k >> bits_y), 1u);
-        k_out[at] = k;
-        v_out[at] = (u32)i;
+        const bool valid = i < n;
+        const u64 k = valid ? key[i] : 0;
+        const u32 col = valid ? (u32)(k >> bits_y) : 0xffffffffu;
+        const u32 peers = __match_any_sync(kFull, col);
+        const int leader = __ffs(peers) - 1;
+        u32 at = 0;
+        if (valid && lane == leader) at = atomicAdd(cursor + col, (u32)__popc(peers));
+        at = __shfl_sync(kFull, at, leader) + __popc(peers & ((1u << lane) - 1));
+        if (valid) {
+            k_out[at] = k;
+            v_out[at] = (u32)i;
+        }
+    }
+}
+
+// Sort each column by row (columns of <= 256 tiles): one warp per column,
+// bitonic network in registers (<= 32) or in the warp's shared buffer.
+constexpr int kColSortMax = 256;
+__global__ void __launch_bounds__(256) k_col_sort(const u32* off, u64 cols, const u64* k_in,
+                                                  const u32* v_in, u64* k_out, u32* v_out) {
+    __shared__ u64 s_k[8][kColSortMax];
+    __shared__ u32 s_v[8][kColSortMax];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64* sk = s_k[wid];
+    u32* sv = s_v[wid];
+    for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c < cols;
+         c += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32 b = off[c], e = off[c + 1];
+        const u32 n = e - b;
+        if (n == 0) continue;
+        if (n == 1) {
+            if (lane == 0) {
+                k_out[b] = k_in[b];
+                v_out[b] = v_in[b];
+            }
+            continue;
+        }
+        if (n <= 32) {
+            u64 k = lane < (int)n ? k_in[b + lane] : ~0ull;
+            u32 v = lane < (int)n ? v_in[b + lane] : 0;
+#pragma unroll
+            for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    const u64 ok = __shfl_xor_sync(kFull, k, stride);
+                    const u32 ov = __shfl_xor_sync(kFull, v, stride);
+                    const bool up = ((lane & size) == 0);
+                    const bool lower = (lane & stride) == 0;
+                    const bool take = lower ? (up ? ok < k : ok > k) : (up ? ok > k : ok < k);
+                    if (take) {
+                        k = ok;
+                        v = ov;
+                    }
+                }
+            }
+            if (lane < (int)n) {
+                k_out[b + lane] = k;
+                v_out[b + lane] = v;
+            }
+            continue;
+        }
+        u32 N = 64;
+        while (N < n) N <<= 1;
+        for (u32 q = lane; q < N; q += 32) {
+            sk[q] = q < n ? k_in[b + q] : ~0ull;
+            sv[q] = q < n ? v_in[b + q] : 0;
+        }
+        __syncwarp();
+        for (u32 size = 2; size <= N; size <<= 1)
+            for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
+                for (u32 q = lane; q < N; q += 32) {
+                    const u32 p = q ^ stride;
+                    if (p > q) {
+                        const bool up = (q & size) == 0;
+                        const u64 a = sk[q], bb = sk[p];
+                        if (up ? a > bb : a < bb) {
+                            sk[q] = bb;
+                            sk[p] = a;
+                            const u32 t = sv[q];
+                            sv[q] = sv[p];
+                            sv[p] = t;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (u32 q = lane; q < n; q += 32) {
+            k_out[b + q] = sk[q];
+            v_out[b + q] = sv[q];
+        }
+        __syncwarp();
     }
 }
 
@@ -451,17 +554,31 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     const u64 cols = sorted_columns(L.key_bits - L.bits_y);
     if (cols && L.col_cnt) {
         cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
-        k_col_hist<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt);
+        cudaMemsetAsync(&L.ctr->max_col, 0, sizeof(u64), st);
+        k_col_hist<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt,
+                                       (u32*)&L.ctr->max_col);
         e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
         if (e != cudaSuccess) return e;
         cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
                         st);
         k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
                                           L.iota);
-        bytes = L.temp_bytes;
-        e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
-                                                (int)n, (int)cols, L.col_off, L.col_off + 1, st);
+        u64 max_col = 0;
+        cudaMemcpyAsync(&max_col, &L.ctr->max_col, sizeof(u64), cudaMemcpyDeviceToHost, st);
+        e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
+        if (max_col <= (u64)kColSortMax) {
+            const u64 want = (cols * 32 + 255) / 256;
+            const u64 capb = (u64)L.n_sm * 8;
+            k_col_sort<<<(int)(want < capb ? (want ? want : 1) : capb), 256, 0, st>>>(
+                L.col_off, cols, L.ktmp, L.iota, L.skey, L.perm);
+        } else {
+            bytes = L.temp_bytes;
+            e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
+                                                    (int)n, (int)cols, L.col_off, L.col_off + 1,
+                                                    st);
+            if (e != cudaSuccess) return e;
+        }
     } else {
         e = launch_iota(L.iota, n, L.n_sm, st);
         if (e != cudaSuccess) return e;

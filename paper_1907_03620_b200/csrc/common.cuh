@@ -207,7 +207,8 @@ struct Counters {
     u64 n_kept;          // clusters after the mu filter
     u64 first_oob;       // strict policy: smallest out-of-bounds index
     u64 n_edges;         // deferred union edges (K3)
-    u64 pad2[11];
+    u64 max_col;         // largest column of significant tiles (sorted K3)
+    u64 pad2[10];
 };
 
 struct Partial {
