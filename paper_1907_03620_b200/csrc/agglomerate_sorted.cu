@@ -444,6 +444,10 @@ __global__ void k_col_scatter(const u64* key, const u64* n_p, u32 bits_y, u32* c
 // Sort each column by row (columns of <= 256 tiles): one warp per column,
 // bitonic network in registers (<= 32) or in the warp's shared buffer.
 constexpr int kColSortMax = 256;
+// Measured on config 4 (8.75M tiles, ~360K columns): CUB's segmented sort
+// 211 us, this warp-per-column kernel 287 us (latency-bound on tiny
+// columns), so it is off by default.
+constexpr bool kUseWarpColumnSort = false;
 __global__ void __launch_bounds__(256) k_col_sort(const u32* off, u64 cols, const u64* k_in,
                                                   const u32* v_in, u64* k_out, u32* v_out) {
     __shared__ u64 s_k[8][kColSortMax];
@@ -567,7 +571,7 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         cudaMemcpyAsync(&max_col, &L.ctr->max_col, sizeof(u64), cudaMemcpyDeviceToHost, st);
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
-        if (max_col <= (u64)kColSortMax) {
+        if (kUseWarpColumnSort && max_col <= (u64)kColSortMax) {
             const u64 want = (cols * 32 + 255) / 256;
             const u64 capb = (u64)L.n_sm * 8;
             k_col_sort<<<(int)(want < capb ? (want ? want : 1) : capb), 256, 0, st>>>(
