@@ -567,10 +567,12 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                         st);
         k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
                                           L.iota);
-        u64 max_col = 0;
-        cudaMemcpyAsync(&max_col, &L.ctr->max_col, sizeof(u64), cudaMemcpyDeviceToHost, st);
-        e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return e;
+        u64 max_col = ~0ull;
+        if (kUseWarpColumnSort) {
+            cudaMemcpyAsync(&max_col, &L.ctr->max_col, sizeof(u64), cudaMemcpyDeviceToHost, st);
+            e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return e;
+        }
         if (kUseWarpColumnSort && max_col <= (u64)kColSortMax) {
             const u64 want = (cols * 32 + 255) / 256;
             const u64 capb = (u64)L.n_sm * 8;
