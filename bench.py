@@ -199,12 +199,18 @@ def ours(args) -> None:
     from paper_1907_03620_b200.raster import Pipeline
 
     rank, local, world = dist_env()
+    # RG_BENCH_BACKEND=gloo RG_BENCH_SAME_GPU=1: exercise the N>1 code path
+    # with several ranks on one GPU (a functional check, never a measurement)
+    backend = os.environ.get("RG_BENCH_BACKEND", "nccl")
+    if os.environ.get("RG_BENCH_SAME_GPU"):
+        local = 0
     torch.cuda.set_device(local)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
 
-        dist_mod.init_process_group("nccl")
+        dist_mod.init_process_group(backend)
         dist = dist_mod
     cfg = args.config
     s = D.spec(cfg)
@@ -221,8 +227,28 @@ def ours(args) -> None:
     t_gen = time.perf_counter() - t0
     dev = host.to(f"cuda:{local}", non_blocking=False)
     stream = torch.cuda.current_stream()
-    pl = Pipeline(gp, device=local)
-    pl.set_stream(stream.cuda_stream)
+    if world == 1:
+        pl = Pipeline(gp, device=local)
+        pl.set_stream(stream.cuda_stream)
+        result_ctx = pl.ctx
+        launches_of = pl.launches
+    else:
+        # N>1: the union of all ranks' shards is clustered (exchange by tile
+        # owner, prune, all-gather of the significant set; distributed.py)
+        from paper_1907_03620_b200.distributed import DistributedPipeline
+
+        pl = DistributedPipeline(gp, device=local, stream=stream.cuda_stream)
+        result_ctx = pl.engine.agg
+        launches_of = pl.engine.launches
+
+    def step_stats(ret):
+        """(ms_contract, rg_stats-like facts) of the step just run."""
+        if world == 1:
+            return ret.ms_contract, ret
+        loc, agg = pl.engine.local.stats(), result_ctx.stats()
+        agg.ms_contract, agg.peak_accumulator_entries = loc.ms_contract, loc.peak_accumulator_entries
+        agg.ms_prune = pl.engine.owner.stats().ms_prune
+        return loc.ms_contract, agg
 
     def barrier():
         if dist:
@@ -232,7 +258,7 @@ def ours(args) -> None:
     for _ in range(args.warmup):
         pl.run(dev)
     barrier()
-    launches0 = pl.launches()
+    launches0 = launches_of()
     ms_contract = []
     st = None
     with ClockSampler(local) as clk:
@@ -241,14 +267,14 @@ def ours(args) -> None:
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            st = pl.run(dev)
-            ms_contract.append(st.ms_contract)
+            mc, st = step_stats(pl.run(dev))
+            ms_contract.append(mc)
         e1.record(stream)
         barrier()
-    launches = pl.launches() - launches0
+    launches = launches_of() - launches0
     ms = e0.elapsed_time(e1)
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -270,20 +296,20 @@ def ours(args) -> None:
     f0.record(stream)
     for _ in range(e2e_steps):
         pl.run(host)
-        pl.ctx.check(pl.ctx.lib.rg_get_significant(pl.ctx.h, tx.ctypes.data, ty.ctypes.data,
-                                                   cnt.ctypes.data, cid.ctypes.data, S,
-                                                   N.RG_MEM_HOST))
+        result_ctx.check(result_ctx.lib.rg_get_significant(
+            result_ctx.h, tx.ctypes.data, ty.ctypes.data, cnt.ctypes.data, cid.ctypes.data, S,
+            N.RG_MEM_HOST))
     f1.record(stream)
     barrier()
     ms_e2e = f0.elapsed_time(f1) / e2e_steps
     if dist:
-        t = torch.tensor([ms_e2e], device="cuda")
+        t = torch.tensor([ms_e2e], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     e2e_value = n * world / (ms_e2e / 1e3)
 
     extra = {}
-    if not args.quick and rank == 0:
+    if not args.quick and world == 1:
         # point-retaining variant: + per-point int32 labels (20 B/pt algorithmic)
         labels = torch.empty(n, dtype=torch.int32, device=dev.device)
         pl.run(dev)
@@ -314,7 +340,9 @@ def ours(args) -> None:
         "config": {"workload": WORKLOADS[cfg], "order": args.order, "points": n * world,
                    "l2": "inputs 8 GB >> 126 MB L2 each step (no flush needed)" if n >= 100_000_000
                    else "inputs smaller than L2: not flushed",
-                   "parallelism": "1 GPU" if world == 1 else f"{world} ranks, independent shards (no cross-rank merge)"},
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"{world} ranks: own shard each, counts exchanged by tile owner "
+                   "(NCCL all_to_all), significant set all-gathered, K3 on every rank"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": k1_traffic(n) if cfg == 4 else None,
                      "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01)",

@@ -130,6 +130,11 @@ const char* rg_last_error(const rg_ctx* ctx);
 rg_status rg_set_stream(rg_ctx* ctx, void* stream);
 rg_status rg_synchronize(rg_ctx* ctx);
 
+/* Empty the context into a fresh accumulator (as constructing a new
+ * TileAccumulator, accumulator.hpp:111-115), keeping its device buffers for
+ * reuse: counts, totals, significant set and clusters are discarded. */
+rg_status rg_reset(rg_ctx* ctx);
+
 /* TileAccumulator::ingest accumulator.hpp:117-134 (+ io.hpp:226-241).
  * Repeatable; chunks may come in any order and partition. Skip policy:
  * out-of-bounds points (closed canvas, NaN included) are counted in
@@ -141,6 +146,25 @@ rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind);
 /* TileAccumulator::merge accumulator.hpp:137-154: folds src into dst (counts
  * add); src is left empty. Both must have equal params. */
 rg_status rg_merge(rg_ctx* dst, rg_ctx* src);
+
+/* Packed tile keys (see rg_device_view) of the accumulator's grid:
+ * key = (tx - origin_x) << bits_y | (ty - origin_y). */
+rg_status rg_key_packing(rg_ctx* ctx, int64_t* origin_x, int64_t* origin_y, uint32_t* bits_y);
+
+/* Entries of the accumulator as (packed key, count) pairs, unsorted — the
+ * for_each_count view (accumulator.hpp:188-191) in a form that can be
+ * exchanged between accumulators (multi-GPU merge). *n_out = D; cap = 0
+ * only queries D, 0 < cap < D is RG_ERR_ARG with nothing written. keys and
+ * counts share `kind`. */
+rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint64_t cap,
+                            uint64_t* n_out, rg_memkind kind);
+
+/* Adds (packed key, count) pairs produced by rg_export_entries of an
+ * accumulator with equal params: the counts-add half of
+ * TileAccumulator::merge (accumulator.hpp:137-154) for pairs that arrive
+ * over the network. total_ingested grows by the summed counts. */
+rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts,
+                           uint64_t n, rg_memkind kind);
 
 /* Accessors (accumulator.hpp:176-197). */
 rg_status rg_entry_count(rg_ctx* ctx, uint64_t* out);      /* :177 */

@@ -107,8 +107,12 @@ GPU_SYMBOLS = {
     "rg_last_error": (C.c_char_p, [P]),
     "rg_set_stream": (ST, [P, P]),
     "rg_synchronize": (ST, [P]),
+    "rg_reset": (ST, [P]),
     "rg_ingest": (ST, [P, P, U64, ST]),
     "rg_merge": (ST, [P, P]),
+    "rg_key_packing": (ST, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_uint32)]),
+    "rg_export_entries": (ST, [P, P, P, U64, C.POINTER(U64), ST]),
+    "rg_ingest_counts": (ST, [P, P, P, U64, ST]),
     "rg_entry_count": (ST, [P, C.POINTER(U64)]),
     "rg_total_ingested": (ST, [P, C.POINTER(U64)]),
     "rg_skipped": (ST, [P, C.POINTER(U64)]),

@@ -23,6 +23,8 @@
 //   5. order   — the C kept roots (C <= S) are radix-sorted by min_key; the
 //                rank is the canonical cluster id (:189-190).
 //   6. label   — every tile gets the id of its root (or -1).
+#include <climits>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -389,6 +391,32 @@ __global__ void k_load_tiles(const long long* tx, const long long* ty, const u64
     }
 }
 
+// Extents of a device tile set (decides the key packing of the load path):
+// out = {min x, max x, min y, max y}, preset by the caller to +inf/-inf.
+__global__ void k_tile_extents(const long long* tx, const long long* ty, u64 n, long long* out) {
+    long long mnx = LLONG_MAX, mxx = LLONG_MIN, mny = LLONG_MAX, mxy = LLONG_MIN;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const long long x = tx[i], y = ty[i];
+        mnx = min(mnx, x);
+        mxx = max(mxx, x);
+        mny = min(mny, y);
+        mxy = max(mxy, y);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mnx = min(mnx, __shfl_xor_sync(~0u, mnx, o));
+        mxx = max(mxx, __shfl_xor_sync(~0u, mxx, o));
+        mny = min(mny, __shfl_xor_sync(~0u, mny, o));
+        mxy = max(mxy, __shfl_xor_sync(~0u, mxy, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&out[0], mnx);
+        atomicMax(&out[1], mxx);
+        atomicMin(&out[2], mny);
+        atomicMax(&out[3], mxy);
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 
 static int grid_for(u64 n, int n_sm, int per_sm = 8) {
@@ -446,6 +474,12 @@ cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u6
     k_load_tiles<<<grid_for(n, n_sm), 256, 0, st>>>(tx, ty, cnt, n, ox, oy, bits_y, t, sig_key,
                                                      sig_cnt, parent, size, npts, min_key,
                                                      root_cid);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_extents(const long long* tx, const long long* ty, u64 n, long long* out,
+                                int n_sm, cudaStream_t st) {
+    k_tile_extents<<<grid_for(n, n_sm, 4), 256, 0, st>>>(tx, ty, n, out);
     return cudaGetLastError();
 }
 

@@ -4,6 +4,7 @@
 // staging, and small utility kernels. No CPU fallback anywhere: every
 // computational entry point runs on the device or fails.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1152,6 +1153,81 @@ rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
     return RG_OK;
 }
 
+rg_status rg_key_packing(rg_ctx* ctx, int64_t* origin_x, int64_t* origin_y, uint32_t* bits_y) {
+    if (!ctx) return RG_ERR_ARG;
+    if (origin_x) *origin_x = ctx->grid.origin_x;
+    if (origin_y) *origin_y = ctx->grid.origin_y;
+    if (bits_y) *bits_y = ctx->grid.bits_y;
+    return RG_OK;
+}
+
+rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint64_t cap,
+                            uint64_t* n_out, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    const u64 d = (ctx->state == rg_ctx::kAccum && ctx->slots) ? ctx->used : 0;
+    if (n_out) *n_out = d;
+    if (d == 0 || cap == 0) return RG_OK;
+    if (cap < d) return set_err(ctx, RG_ERR_ARG, "export buffer holds %llu of %llu entries",
+                                (unsigned long long)cap, (unsigned long long)d);
+    if (!keys || !counts) return set_err(ctx, RG_ERR_ARG, "null buffer");
+    DevGuard guard(ctx->device);
+    u64 *dk = (u64*)keys, *dc = (u64*)counts;
+    if (kind == RG_MEM_HOST) {
+        CK(dalloc(&dk, d));
+        CK(dalloc(&dc, d));
+    }
+    CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(u64), ctx->st));
+    CK(launch_export(ctx->slots, ctx->cap, dk, dc, ctx->scratch, ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    if (kind == RG_MEM_HOST) {
+        CK(cudaMemcpyAsync(keys, dk, d * 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(counts, dc, d * 8, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    if (kind == RG_MEM_HOST) {
+        dfree(dk);
+        dfree(dc);
+    }
+    return RG_OK;
+}
+
+rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts,
+                           uint64_t n, rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && (!keys || !counts)) return set_err(ctx, RG_ERR_ARG, "null buffer");
+    DevGuard guard(ctx->device);
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    if (n == 0) return RG_OK;
+    const u64 need = (u64)((double)(ctx->used + n) / kMaxLoad) + 1;
+    if (!ctx->slots || ctx->cap < need) {
+        s = grow_table(ctx, next_pow2(std::max<u64>(need, 1024)));
+        if (s != RG_OK) return s;
+    }
+    const u64 *dk = (const u64*)keys, *dc = (const u64*)counts;
+    u64 *tk = nullptr, *tc = nullptr;
+    if (kind == RG_MEM_HOST) {
+        CK(dalloc(&tk, n));
+        CK(dalloc(&tc, n));
+        CK(cudaMemcpyAsync(tk, keys, n * 8, cudaMemcpyHostToDevice, ctx->st));
+        CK(cudaMemcpyAsync(tc, counts, n * 8, cudaMemcpyHostToDevice, ctx->st));
+        dk = tk;
+        dc = tc;
+    }
+    CK(cudaMemsetAsync(ctx->scratch, 0, 2 * sizeof(u64), ctx->st));
+    CK(launch_pairs_fold(dk, dc, n, table_of(ctx), ctx->scratch, ctx->scratch + 1, ctx->n_sm,
+                         ctx->st));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(&ctx->hctr->pad0[0], ctx->scratch, 2 * sizeof(u64), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    dfree(tk);
+    dfree(tc);
+    ctx->used += ctx->hctr->pad0[0];
+    ctx->ingested += ctx->hctr->pad0[1];
+    return push_counters(ctx);
+}
+
 rg_status rg_entry_count(rg_ctx* ctx, uint64_t* out) {
     if (!ctx || !out) return RG_ERR_ARG;
     *out = ctx->state == rg_ctx::kAccum ? ctx->used : 0;
@@ -1235,23 +1311,26 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     // Tile extents decide the key packing: the canvas packing when every tile
     // lies on the canvas (then labelling points works), else a packing that
     // covers the tiles' bounding box.
-    std::vector<int64_t> hx, hy;
-    const int64_t* px = tx;
-    const int64_t* py = ty;
-    if (kind == RG_MEM_DEVICE && n) {
-        hx.resize(n);
-        hy.resize(n);
-        CK(cudaMemcpy(hx.data(), tx, n * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hy.data(), ty, n * 8, cudaMemcpyDeviceToHost));
-        px = hx.data();
-        py = hy.data();
-    }
     long long mnx = 0, mxx = 0, mny = 0, mxy = 0;
-    for (u64 i = 0; i < n; ++i) {
-        if (i == 0 || px[i] < mnx) mnx = px[i];
-        if (i == 0 || px[i] > mxx) mxx = px[i];
-        if (i == 0 || py[i] < mny) mny = py[i];
-        if (i == 0 || py[i] > mxy) mxy = py[i];
+    if (kind == RG_MEM_DEVICE && n) {
+        long long* ext = (long long*)&ctx->hctr->pad0[0];  // pinned
+        ext[0] = LLONG_MAX;
+        ext[1] = LLONG_MIN;
+        ext[2] = LLONG_MAX;
+        ext[3] = LLONG_MIN;
+        CK(cudaMemcpyAsync(ctx->scratch, ext, 4 * 8, cudaMemcpyHostToDevice, ctx->st));
+        CK(launch_tile_extents((const long long*)tx, (const long long*)ty, n,
+                               (long long*)ctx->scratch, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        CK(cudaMemcpyAsync(ext, ctx->scratch, 4 * 8, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        mnx = ext[0], mxx = ext[1], mny = ext[2], mxy = ext[3];
+    }
+    for (u64 i = 0; kind != RG_MEM_DEVICE && i < n; ++i) {
+        if (i == 0 || tx[i] < mnx) mnx = tx[i];
+        if (i == 0 || tx[i] > mxx) mxx = tx[i];
+        if (i == 0 || ty[i] < mny) mny = ty[i];
+        if (i == 0 || ty[i] > mxy) mxy = ty[i];
     }
     const Grid& g = ctx->grid;
     Grid res = g;
@@ -1287,24 +1366,30 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     s = ensure_sig_capacity(ctx, n);
     if (s != RG_OK) return s;
     if (n) {
-        long long *dtx = nullptr, *dty = nullptr;
-        u64* dcnt = nullptr;
-        CK(dalloc(&dtx, n));
-        CK(dalloc(&dty, n));
-        if (count) CK(dalloc(&dcnt, n));
-        const cudaMemcpyKind mk =
-            kind == RG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-        CK(cudaMemcpyAsync(dtx, tx, n * 8, mk, ctx->st));
-        CK(cudaMemcpyAsync(dty, ty, n * 8, mk, ctx->st));
-        if (count) CK(cudaMemcpyAsync(dcnt, count, n * 8, mk, ctx->st));
+        const long long* dtx = (const long long*)tx;
+        const long long* dty = (const long long*)ty;
+        const u64* dcnt = (const u64*)count;
+        long long *htx = nullptr, *hty = nullptr;
+        u64* hcnt = nullptr;
+        if (kind == RG_MEM_HOST) {
+            CK(dalloc(&htx, n));
+            CK(dalloc(&hty, n));
+            CK(cudaMemcpyAsync(htx, tx, n * 8, cudaMemcpyHostToDevice, ctx->st));
+            CK(cudaMemcpyAsync(hty, ty, n * 8, cudaMemcpyHostToDevice, ctx->st));
+            if (count) {
+                CK(dalloc(&hcnt, n));
+                CK(cudaMemcpyAsync(hcnt, count, n * 8, cudaMemcpyHostToDevice, ctx->st));
+            }
+            dtx = htx, dty = hty, dcnt = hcnt;
+        }
         CK(launch_load_tiles(dtx, dty, dcnt, n, res.origin_x, res.origin_y, res.bits_y,
                              table_of(ctx), ctx->sig_key, ctx->sig_cnt, ctx->parent, ctx->size,
                              ctx->npts, ctx->min_key, ctx->root_cid, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
-        dfree(dtx);
-        dfree(dty);
-        dfree(dcnt);
+        dfree(htx);
+        dfree(hty);
+        dfree(hcnt);
     }
     ctx->hctr->n_sig = n;
     CK(cudaMemcpyAsync(&ctx->ctr->n_sig, &ctx->hctr->n_sig, sizeof(u64), cudaMemcpyHostToDevice,
@@ -1347,20 +1432,30 @@ rg_status rg_get_stats(rg_ctx* ctx, rg_stats* out) {
     return RG_OK;
 }
 
+static rg_status reset_impl(rg_ctx* ctx) {
+    ctx->state = rg_ctx::kAccum;
+    ctx->table_dirty = true;
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    ctx->ingested = ctx->skipped = 0;
+    ctx->ms_contract = ctx->ms_prune = ctx->ms_agg = ctx->ms_label = 0;
+    return push_counters(ctx);
+}
+
+rg_status rg_reset(rg_ctx* ctx) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    return reset_impl(ctx);
+}
+
 rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                      rg_stats* stats) {
     if (!ctx) return RG_ERR_ARG;
     if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
     DevGuard guard(ctx->device);
     // cluster_sequential builds a fresh accumulator (pipeline.hpp:98).
-    ctx->state = rg_ctx::kAccum;
-    ctx->table_dirty = true;
-    rg_status s = reopen_accumulator(ctx);
+    rg_status s = reset_impl(ctx);
     if (s != RG_OK) return s;
-    ctx->ingested = ctx->skipped = 0;
-    s = push_counters(ctx);
-    if (s != RG_OK) return s;
-    ctx->ms_contract = ctx->ms_prune = ctx->ms_agg = ctx->ms_label = 0;
     s = ingest_any(ctx, xy, n, kind);
     if (s != RG_OK) return s;
     const u64 peak = ctx->used;

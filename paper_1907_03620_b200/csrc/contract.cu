@@ -415,6 +415,90 @@ __global__ void k_table_fold(const Slot* src, u64 n_src, Table dst, u64* claimed
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(claimed, (u64)w);
 }
 
+// Fold (key, count) pairs into a table (merge of pre-aggregated counts, e.g.
+// received from other ranks). Adds the claimed keys and the summed counts.
+__global__ void k_pairs_fold(const u64* keys, const u64* cnts, u64 n, Table dst, u64* claimed,
+                             u64* points) {
+    u32 local = 0;
+    u64 pts = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        local += table_add(dst, keys[i], cnts[i]) ? 1u : 0u;
+        pts += cnts[i];
+    }
+    const u32 w = __reduce_add_sync(kFull, local);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pts += __shfl_xor_sync(kFull, pts, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (w) atomicAdd(claimed, (u64)w);
+        if (pts) atomicAdd(points, pts);
+    }
+}
+
+// Occupied slots -> (key, count) arrays (block-aggregated append).
+__global__ void __launch_bounds__(256) k_export(const Slot* slots, u64 cap, u64* keys, u64* cnts,
+                                                u64* n_out) {
+    __shared__ u32 s_w[8];
+    __shared__ u64 s_base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int kItems = 8;
+    for (u64 base = blockIdx.x * 256ull * kItems; base < cap; base += (u64)gridDim.x * 256 * kItems) {
+        u64 k[kItems], v[kItems];
+        u32 c = 0;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            const u64 i = base + (u64)j * 256 + threadIdx.x;
+            k[j] = kEmpty;
+            v[j] = 0;
+            if (i < cap) ld_slot(slots + i, k[j], v[j]);
+            c += k[j] != kEmpty;
+        }
+        u32 incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) s_w[wid] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u32 t = 0;
+            for (int q = 0; q < 8; ++q) {
+                const u32 x = s_w[q];
+                s_w[q] = t;
+                t += x;
+            }
+            s_base = t ? atomicAdd(n_out, (u64)t) : 0;
+        }
+        __syncthreads();
+        u64 at = s_base + s_w[wid] + incl - c;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j)
+            if (k[j] != kEmpty) {
+                keys[at] = k[j];
+                cnts[at] = v[j];
+                ++at;
+            }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_pairs_fold(const u64* keys, const u64* cnts, u64 n, Table dst, u64* claimed,
+                              u64* points, int n_sm, cudaStream_t st) {
+    const u64 want = (n + 255) / 256;
+    const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
+    k_pairs_fold<<<blocks, 256, 0, st>>>(keys, cnts, n, dst, claimed, points);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export(const Slot* slots, u64 cap, u64* keys, u64* cnts, u64* n_out, int n_sm,
+                          cudaStream_t st) {
+    const u64 want = (cap + 2047) / 2048;
+    const int blocks = (int)(want < (u64)n_sm * 8 ? (want ? want : 1) : (u64)n_sm * 8);
+    k_export<<<blocks, 256, 0, st>>>(slots, cap, keys, cnts, n_out);
+    return cudaGetLastError();
+}
+
 // Strict policy pre-pass: smallest index of an out-of-bounds point.
 __global__ void k_first_oob(const double* xy, u64 n, Grid g, u64* first) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;

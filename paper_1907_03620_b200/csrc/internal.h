@@ -29,6 +29,10 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st);
 cudaError_t launch_table_clear(Slot* slots, u64 n, int n_sm, cudaStream_t st);
 cudaError_t launch_table_fold(const Slot* src, u64 n_src, Table dst, u64* claimed, int n_sm,
                               cudaStream_t st);
+cudaError_t launch_pairs_fold(const u64* keys, const u64* cnts, u64 n, Table dst, u64* claimed,
+                              u64* points, int n_sm, cudaStream_t st);
+cudaError_t launch_export(const Slot* slots, u64 cap, u64* keys, u64* cnts, u64* n_out, int n_sm,
+                          cudaStream_t st);
 cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
@@ -107,6 +111,8 @@ cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u6
                               long long ox, long long oy, u32 bits_y, Table t, u64* sig_key,
                               u64* sig_cnt, u32* parent, u32* size, u64* npts, u64* min_key,
                               int* root_cid, int n_sm, cudaStream_t st);
+cudaError_t launch_tile_extents(const long long* tx, const long long* ty, u64 n, long long* out,
+                                int n_sm, cudaStream_t st);
 
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
                                 int* labels, bool narrow, int n_sm, cudaStream_t st);
