@@ -9,13 +9,13 @@
 //
 //   raster::TileAccumulator        accumulator.hpp:109-214  -> raster::gpu::TileAccumulator
 //   raster::agglomerate            agglomerate.hpp:196-201  -> raster::gpu::agglomerate
+//   raster::window_fix             agglomerate.hpp:212-246  -> raster::gpu::window_fix
 //   raster::cluster_sequential     pipeline.hpp:92-126      -> raster::gpu::cluster_sequential
 //
 // Errors are the reference's exception types (errors.hpp:9-48): status codes
 // map RG_ERR_CONFIG/UNSUPPORTED -> ConfigError, RG_ERR_OOB ->
 // OutOfBoundsError (same message text as accumulator.hpp:124-125), anything
-// else -> Error. Not on the GPU path yet (ConfigError): dedupe_points and
-// use_window_fix.
+// else -> Error. Not on the GPU path yet (ConfigError): dedupe_points.
 #pragma once
 
 #include <algorithm>
@@ -126,8 +126,18 @@ public:
         check(rg_create(&p, device, &ctx_), nullptr);
     }
     ~TileAccumulator() { rg_destroy(ctx_); }
-    TileAccumulator(const TileAccumulator&) = delete;
-    TileAccumulator& operator=(const TileAccumulator&) = delete;
+    /// The reference's accumulator copy (test_agglomerate.cpp:268) on the device.
+    TileAccumulator(const TileAccumulator& o) : params_(o.params_) {
+        check(rg_clone(o.ctx_, &ctx_), nullptr);
+    }
+    TileAccumulator& operator=(const TileAccumulator& o) {
+        if (this != &o) {
+            TileAccumulator tmp(o);
+            std::swap(params_, tmp.params_);
+            std::swap(ctx_, tmp.ctx_);
+        }
+        return *this;
+    }
     TileAccumulator(TileAccumulator&& o) noexcept
         : params_(std::move(o.params_)), ctx_(std::exchange(o.ctx_, nullptr)) {}
     TileAccumulator& operator=(TileAccumulator&& o) noexcept {
@@ -189,6 +199,15 @@ private:
     rg_ctx* ctx_ = nullptr;
 };
 
+/// window_fix agglomerate.hpp:212-246 on the device. The accumulator is
+/// left as it was (the kernel runs on a device copy).
+inline SignificantTiles window_fix(const TileAccumulator& acc, const GridParams& params) {
+    params.validate();
+    TileAccumulator work(acc);
+    check(rg_window_fix(work.handle(), nullptr), work.handle());
+    return detail::significant_from(work.handle());
+}
+
 /// agglomerate agglomerate.hpp:196-201 on the device.
 inline ClusterSet agglomerate(SignificantTiles sig, const GridParams& params) {
     params.validate();
@@ -235,7 +254,6 @@ inline ClusterSet agglomerate(SignificantTiles sig, const GridParams& params) {
 inline ClusterSet cluster_sequential(PointSource& src, const GridParams& params,
                                      bool use_window_fix = false, PipelineStats* stats = nullptr) {
     params.validate();
-    if (use_window_fix) throw ConfigError("window_fix is not supported on the GPU path yet");
     using Clock = std::chrono::steady_clock;
     const auto t0 = Clock::now();
     TileAccumulator acc(params);
@@ -259,7 +277,8 @@ inline ClusterSet cluster_sequential(PointSource& src, const GridParams& params,
     check(rg_get_stats(ctx, &st), ctx);
     const std::size_t peak = st.peak_accumulator_entries;
     const std::uint64_t ingested = st.n_ingested, skipped = st.n_skipped;
-    check(rg_prune(ctx, nullptr), ctx);
+    // prune() or window_fix() (pipeline.hpp:103)
+    check(use_window_fix ? rg_window_fix(ctx, nullptr) : rg_prune(ctx, nullptr), ctx);
     const double t_projection = std::chrono::duration<double>(Clock::now() - t0).count();
     const auto t1 = Clock::now();
     check(rg_agglomerate(ctx, nullptr), ctx);

@@ -147,6 +147,11 @@ rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind);
  * add); src is left empty. Both must have equal params. */
 rg_status rg_merge(rg_ctx* dst, rg_ctx* src);
 
+/* Copy of an accumulator (the reference's TileAccumulator copy, e.g.
+ * test_agglomerate.cpp:268): a new context with equal params holding the
+ * same counts and totals. */
+rg_status rg_clone(rg_ctx* src, rg_ctx** out);
+
 /* Packed tile keys (see rg_device_view) of the accumulator's grid:
  * key = (tx - origin_x) << bits_y | (ty - origin_y). */
 rg_status rg_key_packing(rg_ctx* ctx, int64_t* origin_x, int64_t* origin_y, uint32_t* bits_y);
@@ -181,6 +186,13 @@ rg_status rg_export_counts(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* coun
  * rg_ingest starts from an empty table, as after the reference's prune. */
 rg_status rg_prune(rg_ctx* ctx, uint64_t* n_significant);
 
+/* window_fix agglomerate.hpp:212-246, the alternative to rg_prune: an
+ * occupied tile is significant when some 2x2 window containing it holds
+ * >= threshold points (a superset of rg_prune's set). Consumes the
+ * accumulator like rg_prune (the reference's window_fix takes a const
+ * accumulator: run it on an rg_clone to keep the original). */
+rg_status rg_window_fix(rg_ctx* ctx, uint64_t* n_significant);
+
 /* agglomerate(SignificantTiles, params) agglomerate.hpp:196-201 entry with
  * caller-supplied tiles (any order, no duplicates). Replaces whatever the
  * context held. Counts may be NULL. */
@@ -196,6 +208,12 @@ rg_status rg_agglomerate(rg_ctx* ctx, uint64_t* n_clusters);
  * ingest + prune + agglomerate. stats may be NULL. */
 rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                      rg_stats* stats);
+
+/* cluster_sequential with its options (pipeline.hpp:92-108): flags is a
+ * bitwise OR of RG_CLUSTER_* (RG_CLUSTER_WINDOW_FIX = use_window_fix). */
+#define RG_CLUSTER_WINDOW_FIX 1u
+rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
+                        uint32_t flags, rg_stats* stats);
 
 /* Significant tiles after prune/agglomerate, sorted lexicographically by
  * tile (the canonical order of finalize_clusters), with counts and cluster

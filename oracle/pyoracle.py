@@ -73,6 +73,8 @@ def port():
         lib = C.CDLL(str(PORT_LIB))
         P = C.c_void_p
         lib.orc_cluster.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.POINTER(orc_result)]
+        lib.orc_cluster_ex.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.c_int,
+                                       C.POINTER(orc_result)]
         lib.orc_agglomerate.argtypes = [P, P, P, C.c_uint64, C.POINTER(orc_params),
                                         C.POINTER(orc_result)]
         lib.orc_label_points.argtypes = [P, C.c_uint64, C.POINTER(orc_params),
@@ -100,6 +102,8 @@ def ref():
         lib.ref_time_pipeline.restype = C.c_double
         lib.ref_agglomerate.argtypes = [P, P, P, C.c_uint64, C.POINTER(orc_params),
                                         C.POINTER(orc_result)]
+        lib.ref_cluster_window_fix.argtypes = [P, C.c_uint64, C.POINTER(orc_params),
+                                               C.POINTER(orc_result)]
         lib.ref_prime_points.argtypes = [P, C.c_uint64, C.POINTER(orc_params), P, P, P,
                                          C.c_uint64]
         lib.ref_prime_points.restype = C.c_int64
@@ -144,12 +148,12 @@ def _pts(points) -> np.ndarray:
     return a
 
 
-def port_cluster(points, gp) -> Result:
+def port_cluster(points, gp, window_fix: bool = False) -> Result:
     a = _pts(points)
     r = orc_result()
     lib = port()
-    if lib.orc_cluster(a.ctypes.data if a.size else None, a.shape[0], C.byref(make_params(gp)),
-                       C.byref(r)) != 0:
+    if lib.orc_cluster_ex(a.ctypes.data if a.size else None, a.shape[0],
+                          C.byref(make_params(gp)), int(window_fix), C.byref(r)) != 0:
         raise RuntimeError("oracle failed")
     return _take(r, lib.orc_free)
 
@@ -202,6 +206,16 @@ def ref_cluster(points, gp, workers: int = 0) -> tuple[Result, float, float]:
                        workers, C.byref(r), C.byref(tp), C.byref(tc)) != 0:
         raise RuntimeError(lib.ref_last_error().decode())
     return _take(r, lib.ref_free), tp.value, tc.value
+
+
+def ref_cluster_window_fix(points, gp) -> Result:
+    lib = ref()
+    a = _pts(points)
+    r = orc_result()
+    if lib.ref_cluster_window_fix(a.ctypes.data if a.size else None, a.shape[0],
+                                  C.byref(make_params(gp)), C.byref(r)) != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return _take(r, lib.ref_free)
 
 
 def ref_agglomerate(tx, ty, count, gp) -> Result:

@@ -104,6 +104,49 @@ static int counts_add(counts* c, int64_t x, int64_t y, uint64_t by) {
     }
 }
 
+/* TileCounts::count_of accumulator.hpp:53-61, as a slot index (-1: absent) */
+static int64_t counts_find(const counts* c, int64_t x, int64_t y) {
+    uint64_t i = tile_hash(x, y) & c->mask;
+    for (;;) {
+        const slot* s = &c->s[i];
+        if (s->count == 0) return -1;
+        if (s->x == x && s->y == y) return (int64_t)i;
+        i = (i + 1) & c->mask;
+    }
+}
+
+static uint64_t counts_of(const counts* c, int64_t x, int64_t y) {
+    const int64_t i = counts_find(c, x, y);
+    return i < 0 ? 0 : c->s[i].count;
+}
+
+/* window_fix agglomerate.hpp:212-246: every occupied tile visits the four
+ * 2x2 windows anchored at (x+ax, y+ay), ax, ay in {-1, 0} (:216-218); a
+ * window whose total reaches the threshold (:225-226) marks its occupied
+ * tiles (:227-229). The reference's anchors_seen set (:219) only skips
+ * re-evaluating a window; the marked set is the same without it. */
+static unsigned char* window_fix_marks(const counts* c, uint64_t threshold) {
+    unsigned char* keep = (unsigned char*)calloc(c->cap, 1);
+    if (!keep) return NULL;
+    for (uint64_t i = 0; i < c->cap; ++i) {
+        if (c->s[i].count == 0) continue;
+        for (int ax = -1; ax <= 0; ++ax)
+            for (int ay = -1; ay <= 0; ++ay) {
+                const int64_t x0 = c->s[i].x + ax, y0 = c->s[i].y + ay;
+                const int64_t wx[4] = {x0, x0 + 1, x0, x0 + 1};
+                const int64_t wy[4] = {y0, y0, y0 + 1, y0 + 1};
+                uint64_t total = 0;
+                for (int w = 0; w < 4; ++w) total += counts_of(c, wx[w], wy[w]);
+                if (total < threshold) continue;
+                for (int w = 0; w < 4; ++w) {
+                    const int64_t j = counts_find(c, wx[w], wy[w]);
+                    if (j >= 0) keep[j] = 1;
+                }
+            }
+    }
+    return keep;
+}
+
 /* ------------------------------------------------------ agglomerate.hpp */
 
 typedef struct tile {
@@ -265,6 +308,11 @@ static int fill_result(tile* t, uint64_t n, orc_result* out) {
 }
 
 int orc_cluster(const double* xy, uint64_t n, const orc_params* p, orc_result* out) {
+    return orc_cluster_ex(xy, n, p, 0, out);
+}
+
+int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int use_window_fix,
+                   orc_result* out) {
     memset(out, 0, sizeof *out);
     const double s = pow(10.0, p->precision); /* GridParams::scale core.hpp:95 */
     counts c;
@@ -282,19 +330,25 @@ int orc_cluster(const double* xy, uint64_t n, const orc_params* p, orc_result* o
         ++out->n_ingested;
     }
     out->n_distinct = c.used;
-    /* TileAccumulator::prune accumulator.hpp:160-174 */
+    /* TileAccumulator::prune accumulator.hpp:160-174, or window_fix
+     * (pipeline.hpp:103) */
+    unsigned char* keep = NULL;
+    if (use_window_fix && !(keep = window_fix_marks(&c, p->threshold))) return -1;
+#define KEPT(i) (c.s[i].count != 0 && (keep ? keep[i] : c.s[i].count >= p->threshold))
     uint64_t ns = 0;
     for (uint64_t i = 0; i < c.cap; ++i)
-        if (c.s[i].count != 0 && c.s[i].count >= p->threshold) ++ns;
+        if (KEPT(i)) ++ns;
     tile* t = (tile*)malloc((ns ? ns : 1) * sizeof(tile));
     ns = 0;
     for (uint64_t i = 0; i < c.cap; ++i)
-        if (c.s[i].count != 0 && c.s[i].count >= p->threshold) {
+        if (KEPT(i)) {
             t[ns].x = c.s[i].x;
             t[ns].y = c.s[i].y;
             t[ns].count = c.s[i].count;
             ++ns;
         }
+#undef KEPT
+    free(keep);
     free(c.s);
     if (agglomerate_tiles(t, ns, p, &out->n_components, &out->n_clusters)) return -1;
     const int rc = fill_result(t, ns, out);

@@ -103,6 +103,31 @@ int ref_cluster(const double* xy, uint64_t n, const orc_params* p, unsigned work
     }
 }
 
+// cluster_sequential(pts, params, use_window_fix = true) pipeline.hpp:92-126
+// with the significant set of window_fix agglomerate.hpp:212-246.
+int ref_cluster_window_fix(const double* xy, uint64_t n, const orc_params* p, orc_result* out) {
+    try {
+        std::memset(out, 0, sizeof *out);
+        const raster::GridParams params = to_params(p);
+        std::span<const raster::Point> pts(reinterpret_cast<const raster::Point*>(xy), n);
+        raster::TileAccumulator acc(params);
+        acc.ingest(pts);
+        out->n_ingested = acc.total_ingested();
+        out->n_skipped = acc.skipped();
+        out->n_distinct = acc.entry_count();
+        raster::SignificantTiles sig = raster::window_fix(acc, params);
+        std::vector<std::pair<raster::Tile, std::uint64_t>> flat;
+        flat.reserve(sig.size());
+        for (const auto& [t, s] : sig) flat.emplace_back(t, s.count);
+        std::sort(flat.begin(), flat.end());
+        raster::ClusterSet cs = raster::cluster_sequential(pts, params, true, nullptr);
+        return flatten(flat, cs, out);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // Timing only: the reference pipeline, nothing else. Returns total seconds
 // (PipelineStats::t_total) or a negative value on error.
 double ref_time_pipeline(const double* xy, uint64_t n, const orc_params* p, unsigned workers,

@@ -27,4 +27,5 @@ from .raster import (  # noqa: F401
     cluster_sequential,
     device_count,
     neighbor_offsets,
+    window_fix,
 )

@@ -13,6 +13,7 @@ from .build import GEN_LIB, GPU_LIB
 
 RG_OK, RG_ERR_CONFIG, RG_ERR_OOB, RG_ERR_CUDA, RG_ERR_OOM, RG_ERR_STATE, RG_ERR_ARG, RG_ERR_UNSUPPORTED = range(8)
 RG_MEM_HOST, RG_MEM_DEVICE = 0, 1
+RG_CLUSTER_WINDOW_FIX = 1
 
 
 class NativeLibraryMissing(RuntimeError):
@@ -110,6 +111,7 @@ GPU_SYMBOLS = {
     "rg_reset": (ST, [P]),
     "rg_ingest": (ST, [P, P, U64, ST]),
     "rg_merge": (ST, [P, P]),
+    "rg_clone": (ST, [P, C.POINTER(P)]),
     "rg_key_packing": (ST, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_uint32)]),
     "rg_export_entries": (ST, [P, P, P, U64, C.POINTER(U64), ST]),
     "rg_ingest_counts": (ST, [P, P, P, U64, ST]),
@@ -119,9 +121,11 @@ GPU_SYMBOLS = {
     "rg_count_of": (ST, [P, I64, I64, C.POINTER(U64)]),
     "rg_export_counts": (ST, [P, P, P, P, U64, C.POINTER(U64)]),
     "rg_prune": (ST, [P, C.POINTER(U64)]),
+    "rg_window_fix": (ST, [P, C.POINTER(U64)]),
     "rg_load_significant": (ST, [P, P, P, P, U64, ST]),
     "rg_agglomerate": (ST, [P, C.POINTER(U64)]),
     "rg_cluster": (ST, [P, P, U64, ST, C.POINTER(rg_stats)]),
+    "rg_cluster_ex": (ST, [P, P, U64, ST, C.c_uint32, C.POINTER(rg_stats)]),
     "rg_get_significant": (ST, [P, P, P, P, P, U64, ST]),
     "rg_get_clusters": (ST, [P, P, P, P, P, U64, ST]),
     "rg_device_result": (ST, [P, C.POINTER(rg_device_view)]),

@@ -158,6 +158,8 @@ struct rg_ctx {
     Counters* hctr = nullptr;  // pinned mirror
     Partial* part[2] = {nullptr, nullptr};
     u64* scratch = nullptr;  // device scratch words
+    u8* wf_keep = nullptr;   // window_fix flags, one per table slot
+    u64 wf_cap = 0;
 
     u64 used = 0, ingested = 0, skipped = 0, grows = 0;
     enum State { kAccum, kSig, kAgg } state = kAccum;
@@ -674,7 +676,7 @@ bool use_sorted_k3(const rg_ctx* ctx) {
     return ctx->p.distance <= 2 && ctx->used < 0x7fffffffull;  // S <= D = used
 }
 
-rg_status prune_impl(rg_ctx* ctx) {
+rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
     if (ctx->state != rg_ctx::kAccum) {
         // prune() on a consumed accumulator returns nothing (empty table).
         rg_status s = reopen_accumulator(ctx);
@@ -686,7 +688,19 @@ rg_status prune_impl(rg_ctx* ctx) {
     zero_field(ctx, &ctx->ctr->n_sig);
     if (ctx->slots && ctx->used) {
         const bool hash_k3 = !use_sorted_k3(ctx);
-        CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
+        if (window_fix) {
+            if (ctx->wf_cap < ctx->cap) {
+                dfree(ctx->wf_keep);
+                ctx->wf_cap = 0;
+                CK(dalloc(&ctx->wf_keep, ctx->cap));
+                ctx->wf_cap = ctx->cap;
+            }
+            CK(launch_window_mark(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->grid.bits_x,
+                                  ctx->wf_keep, ctx->n_sm, ctx->st));
+            ++ctx->launches;
+        }
+        CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
+                          window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
                           ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
                           ctx->root_cid, ctx->ctr, ctx->n_sm, ctx->st));
         ++ctx->launches;
@@ -1039,6 +1053,7 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->part[0]);
     dfree(ctx->part[1]);
     dfree(ctx->scratch);
+    dfree(ctx->wf_keep);
     dfree(ctx->sig_key);
     dfree(ctx->sig_cnt);
     dfree(ctx->npts);
@@ -1095,6 +1110,40 @@ rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind) 
     if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
     DevGuard guard(ctx->device);
     return ingest_any(ctx, xy, n, kind);
+}
+
+static rg_status clone_into(rg_ctx* ctx, rg_ctx* src) {
+    if (src->state == rg_ctx::kAccum && src->slots && src->used) {
+        CK(dalloc(&ctx->slots, src->cap));
+        ctx->cap = src->cap;
+        CK(cudaStreamSynchronize(src->st));
+        CK(cudaMemcpyAsync(ctx->slots, src->slots, src->cap * sizeof(Slot),
+                           cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->used = src->used;
+    }
+    ctx->ingested = src->ingested;
+    ctx->skipped = src->skipped;
+    rg_status s = push_counters(ctx);
+    if (s != RG_OK) return s;
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+rg_status rg_clone(rg_ctx* src, rg_ctx** out) {
+    if (!src || !out) return set_err(nullptr, RG_ERR_ARG, "null argument");
+    *out = nullptr;
+    rg_ctx* dst = nullptr;
+    rg_status s = rg_create(&src->p, src->device, &dst);
+    if (s != RG_OK) return s;
+    DevGuard guard(src->device);
+    s = clone_into(dst, src);
+    if (s != RG_OK) {
+        set_err(nullptr, s, "%s", rg_last_error(dst));
+        rg_destroy(dst);
+        return s;
+    }
+    *out = dst;
+    return RG_OK;
 }
 
 rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
@@ -1302,6 +1351,14 @@ rg_status rg_prune(rg_ctx* ctx, uint64_t* n_significant) {
     return s;
 }
 
+rg_status rg_window_fix(rg_ctx* ctx, uint64_t* n_significant) {
+    if (!ctx) return RG_ERR_ARG;
+    DevGuard guard(ctx->device);
+    rg_status s = prune_impl(ctx, true);
+    if (s == RG_OK && n_significant) *n_significant = ctx->n_sig;
+    return s;
+}
+
 rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
                               const uint64_t* count, uint64_t n, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;
@@ -1450,7 +1507,14 @@ rg_status rg_reset(rg_ctx* ctx) {
 
 rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                      rg_stats* stats) {
+    return rg_cluster_ex(ctx, xy, n, kind, 0u, stats);
+}
+
+rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
+                        uint32_t flags, rg_stats* stats) {
     if (!ctx) return RG_ERR_ARG;
+    if (flags & ~(uint32_t)RG_CLUSTER_WINDOW_FIX)
+        return set_err(ctx, RG_ERR_ARG, "unknown rg_cluster_ex flags 0x%x", flags);
     if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
     DevGuard guard(ctx->device);
     // cluster_sequential builds a fresh accumulator (pipeline.hpp:98).
@@ -1459,7 +1523,7 @@ rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
     s = ingest_any(ctx, xy, n, kind);
     if (s != RG_OK) return s;
     const u64 peak = ctx->used;
-    s = prune_impl(ctx);
+    s = prune_impl(ctx, (flags & RG_CLUSTER_WINDOW_FIX) != 0);
     if (s != RG_OK) return s;
     s = agglomerate_impl(ctx);
     if (s != RG_OK) return s;

@@ -37,6 +37,7 @@ namespace rg {
 
 typedef unsigned long long u64;
 typedef unsigned int u32;
+typedef unsigned char u8;
 
 constexpr u64 kEmpty = ~0ull;
 constexpr u64 kSigBit = 1ull << 63;

@@ -558,8 +558,51 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, K2Out out,
-                                                 Counters* ctr) {
+// window_fix agglomerate.hpp:212-246 — a tile is significant when some 2x2
+// window containing it holds >= tau points. The windows containing tile t are
+// the four anchored at t + (ax, ay), ax, ay in {-1, 0}, so the decision for
+// t needs only the counts of its 3x3 neighbourhood: one thread per occupied
+// slot, eight table lookups, one flag byte. (The reference marks every
+// occupied tile of each window it evaluates; the set of marked tiles is the
+// same, since every window containing t is one of t's own four.)
+__global__ void __launch_bounds__(256) k_window_mark(Table t, u64 cap, u64 tau, u32 bits_x,
+                                                     u8* keep) {
+    const long long xlim = 1ll << bits_x, ylim = 1ll << t.bits_y;
+    const u64 ymask = (1ull << t.bits_y) - 1;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < cap;
+         i += (u64)gridDim.x * blockDim.x) {
+        u64 k, v;
+        ld_slot(t.slots + i, k, v);
+        if (k == kEmpty) continue;
+        const long long kx = (long long)(k >> t.bits_y), ky = (long long)(k & ymask);
+        u64 c[3][3];
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy) {
+                u64 w = 0;
+                const long long nx = kx + dx, ny = ky + dy;
+                if (dx == 0 && dy == 0) {
+                    w = v;
+                } else if (nx >= 0 && nx < xlim && ny >= 0 && ny < ylim) {
+                    const u64 f = table_find(t, ((u64)nx << t.bits_y) | (u64)ny);
+                    w = f == kEmpty ? 0 : f;
+                }
+                c[dx + 1][dy + 1] = w;
+            }
+        bool any = false;
+#pragma unroll
+        for (int ax = 0; ax <= 1; ++ax)
+#pragma unroll
+            for (int ay = 0; ay <= 1; ++ay)
+                any |= c[ax][ay] + c[ax + 1][ay] + c[ax][ay + 1] + c[ax + 1][ay + 1] >= tau;
+        keep[i] = any;
+    }
+}
+
+// keep == nullptr: count >= tau (prune); else the window_fix flags.
+__global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, const u8* keep,
+                                                 K2Out out, Counters* ctr) {
     __shared__ u32 s_stage[8][kK2Stage];
     const int lane = threadIdx.x & 31;
     u32* s_idx = s_stage[threadIdx.x >> 5];
@@ -574,6 +617,7 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, K2Ou
             const u64 i = base + j * 32 + lane;
             if (i < cap) {
                 ld_slot(t.slots + i, k[j], v[j]);
+                if (keep) v[j] = keep[i] ? tau : 0;  // predicate only; k2_flush re-reads
             } else {
                 k[j] = kEmpty;
                 v[j] = 0;
@@ -677,14 +721,22 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
     return cudaGetLastError();
 }
 
-cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
-                           int n_sm, cudaStream_t st) {
+cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
+                           u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
+                           Counters* ctr, int n_sm, cudaStream_t st) {
     const u64 per_block = 256ull * kK2Items;
     const u64 want = (cap + per_block - 1) / per_block;
     const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
     const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid};
-    k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, o, ctr);
+    k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, keep, o, ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window_mark(Table t, u64 cap, u64 tau, u32 bits_x, u8* keep, int n_sm,
+                               cudaStream_t st) {
+    const u64 want = (cap + 255) / 256;
+    const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
+    k_window_mark<<<blocks, 256, 0, st>>>(t, cap, tau, bits_x, keep);
     return cudaGetLastError();
 }
 

@@ -35,9 +35,11 @@ cudaError_t launch_export(const Slot* slots, u64 cap, u64* keys, u64* cnts, u64*
                           cudaStream_t st);
 cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
                              cudaStream_t st);
-cudaError_t launch_compact(Table t, u64 cap, u64 tau, u64* sig_key, u64* sig_cnt, u32* parent,
-                           u32* size, u64* npts, u64* min_key, int* root_cid, Counters* ctr,
-                           int n_sm, cudaStream_t st);
+cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
+                           u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
+                           Counters* ctr, int n_sm, cudaStream_t st);
+cudaError_t launch_window_mark(Table t, u64 cap, u64 tau, u32 bits_x, u8* keep, int n_sm,
+                               cudaStream_t st);
 
 struct AggLaunch {
     const u64* sig_key;

@@ -335,6 +335,19 @@ class TileAccumulator:
         tx, ty, cnt, _ = self._ctx.significant_arrays(False)
         return SignificantTiles(tx, ty, cnt, self._ctx)
 
+    def copy(self) -> "TileAccumulator":
+        """The reference's TileAccumulator copy (test_agglomerate.cpp:268)."""
+        out = TileAccumulator.__new__(TileAccumulator)
+        out._params = self._params
+        h = C.c_void_p()
+        self._ctx.check(self._ctx.lib.rg_clone(self._ctx.h, C.byref(h)))
+        ctx = _Context.__new__(_Context)
+        ctx.h, ctx.lib, ctx.params = h, self._ctx.lib, self._params
+        out._ctx = ctx
+        return out
+
+    __copy__ = copy
+
     def entry_count(self) -> int:
         return self._ctx.u64(self._ctx.lib.rg_entry_count)
 
@@ -368,6 +381,16 @@ class TileAccumulator:
 
     def skipped(self) -> int:
         return self._ctx.u64(self._ctx.lib.rg_skipped)
+
+
+def window_fix(acc: TileAccumulator, params: GridParams) -> SignificantTiles:
+    """window_fix agglomerate.hpp:212-246 on the device: occupied tiles with
+    a 2x2 window of >= threshold points. Like the reference it leaves `acc`
+    untouched (it runs on a device copy)."""
+    work = acc.copy()
+    work._ctx.check(work._ctx.lib.rg_window_fix(work._ctx.h, None))
+    tx, ty, cnt, _ = work._ctx.significant_arrays(False)
+    return SignificantTiles(tx, ty, cnt, work._ctx)
 
 
 # ----------------------------------------------------------- agglomerate.hpp
@@ -473,12 +496,14 @@ class Pipeline:
     def set_stream(self, stream_ptr: int | None) -> None:
         self.ctx.check(self.ctx.lib.rg_set_stream(self.ctx.h, stream_ptr))
 
-    def run(self, pts) -> N.rg_stats:
+    def run(self, pts, use_window_fix: bool = False) -> N.rg_stats:
         """cluster_sequential pipeline.hpp:92-126 on the device; results stay
         resident (device_view / flat / labels)."""
         p = _Points(pts)
         s = N.rg_stats()
-        self.ctx.check(self.ctx.lib.rg_cluster(self.ctx.h, p.ptr, p.n, p.kind, C.byref(s)))
+        flags = N.RG_CLUSTER_WINDOW_FIX if use_window_fix else 0
+        self.ctx.check(self.ctx.lib.rg_cluster_ex(self.ctx.h, p.ptr, p.n, p.kind, flags,
+                                                  C.byref(s)))
         return s
 
     def device_view(self) -> N.rg_device_view:
@@ -509,9 +534,10 @@ class Pipeline:
         return int(self.ctx.lib.rg_kernel_launches(self.ctx.h))
 
 
-def cluster_flat(pts, params: GridParams, device: int = -1) -> FlatClustering:
+def cluster_flat(pts, params: GridParams, device: int = -1,
+                 use_window_fix: bool = False) -> FlatClustering:
     pl = Pipeline(params, device)
-    pl.run(pts)
+    pl.run(pts, use_window_fix)
     return pl.flat()
 
 
@@ -520,12 +546,10 @@ def cluster_sequential(pts, params: GridParams, use_window_fix: bool = False,
     """cluster_sequential pipeline.hpp:92-126 (count-only clustering on the
     device). In retain_points mode every cluster's points are attached
     (sorted by point_less, core.hpp:22-24) from the per-point labels."""
-    if use_window_fix:
-        raise ConfigError("window_fix is not supported on the GPU path yet")
     params.validate()
     pl = Pipeline(params)
     p = _Points(pts)
-    pl.run(pts)
+    pl.run(pts, use_window_fix)
     flat = pl.flat()
     if stats is not None:
         st = pl.ctx.stats()

@@ -149,7 +149,36 @@ int main() {
         try { raster::gpu::TileAccumulator(params).ingest(pts); } catch (const OutOfBoundsError& e) { b = e.what(); }
         CHECK(!a.empty() && a == b, "strict OutOfBoundsError message");
     }
-    // 6. Config errors are ConfigError.
+    // 6. window_fix (agglomerate.hpp:212-246) and cluster_sequential with
+    //    use_window_fix, against the reference; the accumulator copy and the
+    //    const-ness of window_fix (test_agglomerate.cpp:255-277).
+    {
+        std::mt19937_64 r4(0x3f1c);
+        for (int round = 0; round < 6; ++round) {
+            GridParams params;
+            params.precision = round % 2 ? 3.0 : 2.0;
+            params.threshold = 2 + r4() % 6;
+            params.min_cluster_size = 1 + r4() % 4;
+            const auto pts = gaussian_clusters(100 + r4() % 200, 60, 0.004, r4(), 0.2);
+            raster::TileAccumulator ra(params);
+            raster::gpu::TileAccumulator ga(params);
+            ra.ingest(pts);
+            ga.ingest(pts);
+            const std::size_t before = ga.entry_count();
+            CHECK(sorted_sig(raster::window_fix(ra, params)) ==
+                      sorted_sig(raster::gpu::window_fix(ga, params)),
+                  ("window_fix round " + std::to_string(round)).c_str());
+            CHECK(ga.entry_count() == before, "window_fix leaves the accumulator intact");
+            raster::gpu::TileAccumulator copy = ga;
+            CHECK(sorted_sig(copy.prune()) == sorted_sig(ga.prune()), "copied accumulator");
+            PipelineStats s_ref, s_gpu;
+            CHECK(raster::cluster_sequential(pts, params, true, &s_ref) ==
+                      raster::gpu::cluster_sequential(pts, params, true, &s_gpu),
+                  ("cluster_sequential window_fix round " + std::to_string(round)).c_str());
+            CHECK(s_ref.n_significant == s_gpu.n_significant, "window_fix n_significant");
+        }
+    }
+    // 7. Config errors are ConfigError.
     {
         GridParams bad;
         bad.threshold = 0;

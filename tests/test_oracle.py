@@ -155,3 +155,42 @@ def test_reference_strict_message_format():
     thrown, msg, ing = O.ref_strict(np.array([[0.5, 0.5], [500.0, 0.0], [0.6, 0.6]]),
                                     GridParams(precision=2))
     assert thrown and msg == "point (500.000000, 0.000000) outside canvas bounds" and ing == 1
+
+
+def test_window_fix_kats(kat):
+    """window_fix agglomerate.hpp:212-246 KATs, on the port and (when built)
+    the reference itself."""
+    for c in kat["window_fix"]:
+        gp = GridParams(precision=c["precision"], threshold=c["threshold"], min_cluster_size=1)
+        pts = centre_points(c["tile_copies"], c["precision"])
+        plain = O.port_cluster(pts, gp)
+        fixed = O.port_cluster(pts, gp, window_fix=True)
+        assert [[int(x), int(y)] for x, y in zip(plain.tx, plain.ty)] == c["plain_kept"], c["cite"]
+        assert [[int(x), int(y)] for x, y in zip(fixed.tx, fixed.ty)] == c["window_kept"], c["cite"]
+        if O.ref() is not None:
+            r = O.ref_cluster_window_fix(pts, gp)
+            assert np.array_equal(r.tx, fixed.tx) and np.array_equal(r.ty, fixed.ty)
+            assert np.array_equal(r.cluster_id, fixed.cluster_id)
+
+
+def test_window_fix_superset_and_live_reference():
+    """test_agglomerate.cpp:255-277 (superset of plain pruning, counts equal)
+    plus random inputs against the live reference."""
+    rng = np.random.default_rng(99)
+    for trial in range(6):
+        gp = GridParams(precision=2, threshold=int(rng.integers(2, 7)),
+                        min_cluster_size=int(rng.integers(1, 4)))
+        tiles = rng.integers(0, 31, size=(120, 2))
+        copies = rng.integers(1, 8, size=120)
+        pts = centre_points([((int(a), int(b)), int(k)) for (a, b), k in zip(tiles, copies)], 2)
+        pts = np.concatenate([pts, rng.uniform(0, 0.31, size=(300, 2))])
+        plain = O.port_cluster(pts, gp)
+        fixed = O.port_cluster(pts, gp, window_fix=True)
+        fx = {(int(x), int(y)): int(n) for x, y, n in zip(fixed.tx, fixed.ty, fixed.count)}
+        for x, y, n in zip(plain.tx, plain.ty, plain.count):
+            assert fx[(int(x), int(y))] == int(n)
+        if O.ref() is not None:
+            r = O.ref_cluster_window_fix(pts, gp)
+            assert np.array_equal(r.tx, fixed.tx) and np.array_equal(r.ty, fixed.ty), trial
+            assert np.array_equal(r.count, fixed.count), trial
+            assert np.array_equal(r.cluster_id, fixed.cluster_id), trial
