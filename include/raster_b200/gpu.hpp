@@ -102,17 +102,22 @@ inline ClusterSet clusters_from(rg_ctx* ctx) {
     return cs;
 }
 
-// RASTER' points: every in-bounds point of a kept cluster, sorted by
-// point_less (agglomerate.hpp:183, core.hpp:22-24).
+// RASTER' points: every in-bounds point of a kept cluster, grouped and
+// sorted by point_less on the device (agglomerate.hpp:70-76,183,
+// core.hpp:22-24).
 inline void attach_points(rg_ctx* ctx, std::span<const Point> pts, ClusterSet& cs) {
     if (cs.clusters.empty() || pts.empty()) return;
-    std::vector<std::int32_t> labels(pts.size());
-    check(rg_label_points(ctx, reinterpret_cast<const double*>(pts.data()), pts.size(),
-                          labels.data(), RG_MEM_HOST),
+    std::uint64_t m = 0, c = 0;
+    check(rg_cluster_points(ctx, reinterpret_cast<const double*>(pts.data()), pts.size(),
+                            RG_MEM_HOST, &m, &c),
           ctx);
-    for (std::size_t i = 0; i < pts.size(); ++i)
-        if (labels[i] >= 0) cs.clusters[static_cast<std::size_t>(labels[i])].points.push_back(pts[i]);
-    for (Cluster& c : cs.clusters) std::sort(c.points.begin(), c.points.end(), point_less);
+    std::vector<Point> xy(m);
+    std::vector<std::uint64_t> off(c + 1);
+    check(rg_get_cluster_points(ctx, reinterpret_cast<double*>(xy.data()), m, off.data(),
+                                RG_MEM_HOST),
+          ctx);
+    for (std::uint64_t k = 0; k < c && k < cs.clusters.size(); ++k)
+        cs.clusters[k].points.assign(xy.begin() + off[k], xy.begin() + off[k + 1]);
 }
 
 }  // namespace detail

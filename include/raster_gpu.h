@@ -215,6 +215,22 @@ rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
 rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                         uint32_t flags, rg_stats* stats);
 
+/* RASTER' output (Mode::retain_points: take_points agglomerate.hpp:70-76 and
+ * the point sort of finalize_clusters :183): every in-bounds point of xy
+ * whose tile belongs to a kept cluster, grouped by cluster id and ordered by
+ * point_less (core.hpp:22-24) within a cluster; with dedupe_points, equal
+ * points of a cluster appear once (TileAccumulator::dedupe
+ * accumulator.hpp:199-204). Pass the points that were clustered. Results
+ * stay in the context (*n_points = M, *n_clusters = C) until
+ * rg_get_cluster_points copies them out. n < 2^32 - 1 per call. */
+rg_status rg_cluster_points(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
+                            uint64_t* n_points, uint64_t* n_clusters);
+/* Copies min(cap, M) points (x, y interleaved) and the C + 1 cluster offsets
+ * (cluster k = points [offsets[k], offsets[k+1])). Either pointer may be
+ * NULL; both are `kind` memory. */
+rg_status rg_get_cluster_points(rg_ctx* ctx, double* xy, uint64_t cap, uint64_t* offsets,
+                                rg_memkind kind);
+
 /* Significant tiles after prune/agglomerate, sorted lexicographically by
  * tile (the canonical order of finalize_clusters), with counts and cluster
  * ids (-1: component dropped by the mu filter, or not agglomerated yet).

@@ -131,6 +131,8 @@ GPU_SYMBOLS = {
     "rg_device_result": (ST, [P, C.POINTER(rg_device_view)]),
     "rg_decode_key": (None, [C.POINTER(rg_device_view), U64, C.POINTER(I64), C.POINTER(I64)]),
     "rg_label_points": (ST, [P, P, U64, P, ST]),
+    "rg_cluster_points": (ST, [P, P, U64, ST, C.POINTER(U64), C.POINTER(U64)]),
+    "rg_get_cluster_points": (ST, [P, P, U64, P, ST]),
     "rg_get_stats": (ST, [P, C.POINTER(rg_stats)]),
     "rg_kernel_launches": (U64, [P]),
 }

@@ -158,6 +158,11 @@ struct rg_ctx {
     Counters* hctr = nullptr;  // pinned mirror
     Partial* part[2] = {nullptr, nullptr};
     u64* scratch = nullptr;  // device scratch words
+    // RASTER' cluster points (rg_cluster_points): 2*cp_n doubles, cp_c+1 offsets
+    double* cp_xy = nullptr;
+    u64* cp_off = nullptr;
+    u64 cp_n = 0, cp_c = 0;
+    bool cp_valid = false;
     u8* wf_keep = nullptr;   // window_fix flags, one per table slot
     u64 wf_cap = 0;
 
@@ -691,6 +696,8 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
         if (window_fix) {
             if (ctx->wf_cap < ctx->cap) {
                 dfree(ctx->wf_keep);
+    dfree(ctx->cp_xy);
+    dfree(ctx->cp_off);
                 ctx->wf_cap = 0;
                 CK(dalloc(&ctx->wf_keep, ctx->cap));
                 ctx->wf_cap = ctx->cap;
@@ -1054,6 +1061,8 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->part[1]);
     dfree(ctx->scratch);
     dfree(ctx->wf_keep);
+    dfree(ctx->cp_xy);
+    dfree(ctx->cp_off);
     dfree(ctx->sig_key);
     dfree(ctx->sig_cnt);
     dfree(ctx->npts);
@@ -1694,6 +1703,111 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         CK(cudaMemcpyAsync(labels + off, ctx->lstage[b], len * 4, cudaMemcpyDeviceToHost,
                            ctx->st));
     }
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+rg_status rg_cluster_points(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
+                            uint64_t* n_points, uint64_t* n_clusters) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
+    if (ctx->state != rg_ctx::kAgg)
+        return set_err(ctx, RG_ERR_STATE, "cluster points require rg_agglomerate first");
+    if (!ctx->res_is_canvas)
+        return set_err(ctx, RG_ERR_UNSUPPORTED,
+                       "cluster points need significant tiles on the canvas");
+    if (n >= 0xffffffffull)
+        return set_err(ctx, RG_ERR_UNSUPPORTED, "cluster points: at most 2^32-2 points per call");
+    DevGuard guard(ctx->device);
+    PhaseTimer timer(ctx, &ctx->ms_label);
+    ctx->cp_valid = false;
+    const u64 C = ctx->n_kept;
+    dfree(ctx->cp_xy);
+    dfree(ctx->cp_off);
+    ctx->cp_xy = nullptr;
+    ctx->cp_n = 0;
+    CK(dalloc(&ctx->cp_off, C + 1));
+    CK(cudaMemsetAsync(ctx->cp_off, 0, (C + 1) * sizeof(u64), ctx->st));
+    ctx->cp_c = C;
+    if (n == 0 || C == 0) {
+        CK(cudaStreamSynchronize(ctx->st));
+        ctx->cp_valid = true;
+        if (n_points) *n_points = 0;
+        if (n_clusters) *n_clusters = C;
+        return RG_OK;
+    }
+    // every buffer below is released on every path out of this block
+    struct Tmp {
+        double* xy = nullptr;
+        int* lab = nullptr;
+        u32 *ia = nullptr, *ib = nullptr;
+        u64 *ka = nullptr, *kb = nullptr;
+        void* temp = nullptr;
+        ~Tmp() {
+            dfree(xy);
+            dfree(lab);
+            dfree(ia);
+            dfree(ib);
+            dfree(ka);
+            dfree(kb);
+            if (temp) cudaFree(temp);
+        }
+    } T;
+    const double* dxy = xy;
+    if (kind == RG_MEM_HOST) {
+        CK(dalloc(&T.xy, 2 * n));
+        CK(cudaMemcpyAsync(T.xy, xy, n * 16, cudaMemcpyHostToDevice, ctx->st));
+        dxy = T.xy;
+    }
+    CK(dalloc(&T.lab, n));
+    CK(launch_label_points(dxy, n, ctx->grid, table_of(ctx), ctx->tile_cid, T.lab, ctx->narrow,
+                           ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    CK(dalloc(&T.ia, n));
+    CK(dalloc(&T.ib, n));
+    CK(dalloc(&T.ka, n + 1));
+    CK(dalloc(&T.kb, n + 1));
+    CK(dalloc(&ctx->cp_xy, 2 * n));
+    PointsLaunch L;
+    L.xy = dxy;
+    L.labels = T.lab;
+    L.n = n;
+    L.n_clusters = C;
+    L.dedupe = ctx->p.dedupe_points ? 1 : 0;
+    L.idx_a = T.ia;
+    L.idx_b = T.ib;
+    L.key_a = T.ka;
+    L.key_b = T.kb;
+    L.m_dev = ctx->scratch;
+    L.m_host = &ctx->hctr->pad0[0];
+    L.temp_bytes = cluster_points_temp_bytes(n);
+    CK(cudaMalloc(&T.temp, L.temp_bytes));
+    L.temp = T.temp;
+    L.out_xy = ctx->cp_xy;
+    L.offsets = ctx->cp_off;
+    L.n_sm = ctx->n_sm;
+    CK(launch_cluster_points(L, ctx->st));
+    ctx->launches += 9;
+    CK(cudaMemcpyAsync(&ctx->hctr->pad0[1], ctx->cp_off + C, sizeof(u64), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->cp_n = ctx->hctr->pad0[1];
+    ctx->cp_valid = true;
+    if (n_points) *n_points = ctx->cp_n;
+    if (n_clusters) *n_clusters = C;
+    return RG_OK;
+}
+
+rg_status rg_get_cluster_points(rg_ctx* ctx, double* xy, uint64_t cap, uint64_t* offsets,
+                                rg_memkind kind) {
+    if (!ctx) return RG_ERR_ARG;
+    if (!ctx->cp_valid) return set_err(ctx, RG_ERR_STATE, "call rg_cluster_points first");
+    DevGuard guard(ctx->device);
+    const cudaMemcpyKind mk =
+        kind == RG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const u64 w = std::min<u64>(cap, ctx->cp_n);
+    if (xy && w) CK(cudaMemcpyAsync(xy, ctx->cp_xy, w * 16, mk, ctx->st));
+    if (offsets) CK(cudaMemcpyAsync(offsets, ctx->cp_off, (ctx->cp_c + 1) * 8, mk, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     return RG_OK;
 }

@@ -116,6 +116,26 @@ cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u6
 cudaError_t launch_tile_extents(const long long* tx, const long long* ty, u64 n, long long* out,
                                 int n_sm, cudaStream_t st);
 
+// RASTER' cluster points (points.cu)
+struct PointsLaunch {
+    const double* xy;
+    const int* labels;
+    u64 n;
+    u64 n_clusters;
+    int dedupe;
+    u32 *idx_a, *idx_b;   // n entries each
+    u64 *key_a, *key_b;   // n + 1 entries each
+    u64* m_dev;
+    u64* m_host;          // pinned
+    void* temp;
+    size_t temp_bytes;
+    double* out_xy;       // 2 * M doubles
+    u64* offsets;         // n_clusters + 1
+    int n_sm;
+};
+size_t cluster_points_temp_bytes(u64 m);
+cudaError_t launch_cluster_points(const PointsLaunch& L, cudaStream_t st);
+
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
                                 int* labels, bool narrow, int n_sm, cudaStream_t st);
 

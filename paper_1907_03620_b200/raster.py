@@ -530,6 +530,30 @@ class Pipeline:
         self.ctx.check(self.ctx.lib.rg_label_points(self.ctx.h, p.ptr, p.n, ptr, p.kind))
         return out
 
+    def cluster_points(self, pts, device_out: bool = False):
+        """RASTER' output on the device (take_points agglomerate.hpp:70-76,
+        finalize_clusters :183): (points (M, 2) float64 grouped by cluster id
+        and point_less-sorted within a cluster, offsets (C + 1,) uint64)."""
+        p = _Points(pts)
+        m, c = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.ctx.lib.rg_cluster_points(self.ctx.h, p.ptr, p.n, p.kind,
+                                                      C.byref(m), C.byref(c)))
+        if device_out:
+            import torch
+
+            xy = torch.empty((m.value, 2), dtype=torch.float64, device="cuda")
+            off = torch.empty(c.value + 1, dtype=torch.int64, device="cuda")
+            self.ctx.check(self.ctx.lib.rg_get_cluster_points(
+                self.ctx.h, xy.data_ptr() if m.value else None, m.value, off.data_ptr(),
+                N.RG_MEM_DEVICE))
+            return xy, off
+        xy = np.empty((m.value, 2), np.float64)
+        off = np.empty(c.value + 1, np.uint64)
+        self.ctx.check(self.ctx.lib.rg_get_cluster_points(
+            self.ctx.h, xy.ctypes.data if m.value else None, m.value, off.ctypes.data,
+            N.RG_MEM_HOST))
+        return xy, off
+
     def launches(self) -> int:
         return int(self.ctx.lib.rg_kernel_launches(self.ctx.h))
 
@@ -543,9 +567,9 @@ def cluster_flat(pts, params: GridParams, device: int = -1,
 
 def cluster_sequential(pts, params: GridParams, use_window_fix: bool = False,
                        stats: PipelineStats | None = None) -> ClusterSet:
-    """cluster_sequential pipeline.hpp:92-126 (count-only clustering on the
-    device). In retain_points mode every cluster's points are attached
-    (sorted by point_less, core.hpp:22-24) from the per-point labels."""
+    """cluster_sequential pipeline.hpp:92-126 on the device. In
+    retain_points mode every cluster's points are attached, grouped and
+    point_less-sorted on the device (rg_cluster_points)."""
     params.validate()
     pl = Pipeline(params)
     p = _Points(pts)
@@ -556,19 +580,10 @@ def cluster_sequential(pts, params: GridParams, use_window_fix: bool = False,
         stats._fill(st)
     cs = flat.cluster_set()
     if params.mode == Mode.retain_points and cs.clusters:
-        labels = pl.label_points(p.keep)
-        host = p.keep if isinstance(p.keep, np.ndarray) else p.keep.cpu().numpy()
-        host = host.reshape(-1, 2)
-        if not isinstance(labels, np.ndarray):
-            labels = labels.cpu().numpy()
-        sel = labels >= 0
-        lab, xs, ys = labels[sel], host[sel, 0], host[sel, 1]
-        order = np.lexsort((ys, xs, lab))
-        lab, xs, ys = lab[order], xs[order], ys[order]
-        bounds = np.searchsorted(lab, np.arange(len(cs.clusters) + 1))
+        xy, off = pl.cluster_points(p.keep)
         for k, c in enumerate(cs.clusters):
-            s, e = bounds[k], bounds[k + 1]
-            c.points = list(zip(xs[s:e].tolist(), ys[s:e].tolist()))
+            s, e = int(off[k]), int(off[k + 1])
+            c.points = list(zip(xy[s:e, 0].tolist(), xy[s:e, 1].tolist()))
     return cs
 
 
