@@ -15,7 +15,7 @@
 // Errors are the reference's exception types (errors.hpp:9-48): status codes
 // map RG_ERR_CONFIG/UNSUPPORTED -> ConfigError, RG_ERR_OOB ->
 // OutOfBoundsError (same message text as accumulator.hpp:124-125), anything
-// else -> Error. Not on the GPU path yet (ConfigError): dedupe_points.
+// else -> Error.
 #pragma once
 
 #include <algorithm>

@@ -72,7 +72,8 @@ typedef struct rg_params {
     uint64_t min_cluster_size; /* mu                               default 4   */
     int32_t mode;              /* rg_mode                          count_only  */
     int32_t oob_policy;        /* rg_oob                           skip        */
-    int32_t dedupe_points;     /* must be 0 (dedupe not on the GPU path yet)   */
+    int32_t dedupe_points;     /* retain mode: thresholds and cluster points on
+                                  unique coordinates (accumulator.hpp:199-204) */
     int32_t reserved0;
     uint64_t capacity_hint;    /* expected distinct tiles; 0 = automatic       */
 } rg_params;

@@ -102,8 +102,11 @@ def ref():
         lib.ref_time_pipeline.restype = C.c_double
         lib.ref_agglomerate.argtypes = [P, P, P, C.c_uint64, C.POINTER(orc_params),
                                         C.POINTER(orc_result)]
-        lib.ref_cluster_window_fix.argtypes = [P, C.c_uint64, C.POINTER(orc_params),
-                                               C.POINTER(orc_result)]
+        lib.ref_cluster_flags.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.c_int,
+                                          C.POINTER(orc_result)]
+        lib.ref_prime_points_ex.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.c_int, P, P,
+                                            P, C.c_uint64]
+        lib.ref_prime_points_ex.restype = C.c_int64
         lib.ref_prime_points.argtypes = [P, C.c_uint64, C.POINTER(orc_params), P, P, P,
                                          C.c_uint64]
         lib.ref_prime_points.restype = C.c_int64
@@ -148,12 +151,17 @@ def _pts(points) -> np.ndarray:
     return a
 
 
-def port_cluster(points, gp, window_fix: bool = False) -> Result:
+def _flags(window_fix: bool, dedupe: bool) -> int:
+    return (1 if window_fix else 0) | (2 if dedupe else 0)
+
+
+def port_cluster(points, gp, window_fix: bool = False, dedupe: bool = False) -> Result:
+    """dedupe = Mode::retain_points with dedupe_points."""
     a = _pts(points)
     r = orc_result()
     lib = port()
     if lib.orc_cluster_ex(a.ctypes.data if a.size else None, a.shape[0],
-                          C.byref(make_params(gp)), int(window_fix), C.byref(r)) != 0:
+                          C.byref(make_params(gp)), _flags(window_fix, dedupe), C.byref(r)) != 0:
         raise RuntimeError("oracle failed")
     return _take(r, lib.orc_free)
 
@@ -209,11 +217,16 @@ def ref_cluster(points, gp, workers: int = 0) -> tuple[Result, float, float]:
 
 
 def ref_cluster_window_fix(points, gp) -> Result:
+    return ref_cluster_flags(points, gp, window_fix=True)
+
+
+def ref_cluster_flags(points, gp, window_fix: bool = False, dedupe: bool = False) -> Result:
     lib = ref()
     a = _pts(points)
     r = orc_result()
-    if lib.ref_cluster_window_fix(a.ctypes.data if a.size else None, a.shape[0],
-                                  C.byref(make_params(gp)), C.byref(r)) != 0:
+    if lib.ref_cluster_flags(a.ctypes.data if a.size else None, a.shape[0],
+                             C.byref(make_params(gp)), _flags(window_fix, dedupe),
+                             C.byref(r)) != 0:
         raise RuntimeError(lib.ref_last_error().decode())
     return _take(r, lib.ref_free)
 
@@ -245,20 +258,21 @@ def ref_time(points_ptr: int, n: int, gp, workers: int = 0):
     return t, tp.value, tc.value, nc.value
 
 
-def ref_prime_points(points, gp):
+def ref_prime_points(points, gp, window_fix: bool = False, dedupe: bool = False):
     """Reference RASTER' output rows (cluster id, x, y) in output order."""
     lib = ref()
     a = _pts(points)
     p = make_params(gp)
-    n = lib.ref_prime_points(a.ctypes.data if a.size else None, a.shape[0], C.byref(p),
-                             None, None, None, 0)
+    f = _flags(window_fix, dedupe)
+    n = lib.ref_prime_points_ex(a.ctypes.data if a.size else None, a.shape[0], C.byref(p), f,
+                                None, None, None, 0)
     if n < 0:
         raise RuntimeError(lib.ref_last_error().decode())
     cid = np.empty(n, np.int64)
     px = np.empty(n, np.float64)
     py = np.empty(n, np.float64)
-    lib.ref_prime_points(a.ctypes.data if a.size else None, a.shape[0], C.byref(p),
-                         cid.ctypes.data, px.ctypes.data, py.ctypes.data, n)
+    lib.ref_prime_points_ex(a.ctypes.data if a.size else None, a.shape[0], C.byref(p), f,
+                            cid.ctypes.data, px.ctypes.data, py.ctypes.data, n)
     return cid, px, py
 
 

@@ -307,12 +307,57 @@ static int fill_result(tile* t, uint64_t n, orc_result* out) {
     return 0;
 }
 
+/* dedupe (accumulator.hpp:199-204): unique points per tile, compared with
+ * operator== on doubles (core.hpp:17; -0.0 == +0.0). */
+typedef struct tpt {
+    int64_t tx, ty;
+    double x, y;
+} tpt;
+
+static int cmp_tpt(const void* a, const void* b) {
+    const tpt* p = (const tpt*)a;
+    const tpt* q = (const tpt*)b;
+    const int t = tile_cmp(p->tx, p->ty, q->tx, q->ty);
+    if (t) return t;
+    if (p->x < q->x) return -1;
+    if (p->x > q->x) return 1;
+    if (p->y < q->y) return -1;
+    if (p->y > q->y) return 1;
+    return 0;
+}
+
+static int unique_counts(const double* xy, uint64_t n, const orc_params* p, double s,
+                         counts* u) {
+    tpt* a = (tpt*)malloc((n ? n : 1) * sizeof(tpt));
+    if (!a) return -1;
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double x = xy[2 * i], y = xy[2 * i + 1];
+        if (!contains(p, x, y)) continue;
+        orc_project(x, y, s, &a[m].tx, &a[m].ty);
+        a[m].x = x;
+        a[m].y = y;
+        ++m;
+    }
+    qsort(a, m, sizeof(tpt), cmp_tpt);
+    for (uint64_t i = 0; i < m; ++i) {
+        if (i > 0 && a[i].tx == a[i - 1].tx && a[i].ty == a[i - 1].ty && a[i].x == a[i - 1].x &&
+            a[i].y == a[i - 1].y)
+            continue;
+        if (counts_add(u, a[i].tx, a[i].ty, 1)) return -1;
+    }
+    free(a);
+    return 0;
+}
+
 int orc_cluster(const double* xy, uint64_t n, const orc_params* p, orc_result* out) {
     return orc_cluster_ex(xy, n, p, 0, out);
 }
 
-int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int use_window_fix,
+int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int flags,
                    orc_result* out) {
+    const int use_window_fix = flags & ORC_WINDOW_FIX;
+    const int dedupe = flags & ORC_DEDUPE;
     memset(out, 0, sizeof *out);
     const double s = pow(10.0, p->precision); /* GridParams::scale core.hpp:95 */
     counts c;
@@ -334,6 +379,16 @@ int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int use_wi
      * (pipeline.hpp:103) */
     unsigned char* keep = NULL;
     if (use_window_fix && !(keep = window_fix_marks(&c, p->threshold))) return -1;
+    /* dedupe: the threshold and the reported count use unique points
+     * (accumulator.hpp:165-169); window_fix decides on raw counts (:225). */
+    counts u;
+    u.s = NULL;
+    if (dedupe) {
+        if (counts_init(&u) || unique_counts(xy, n, p, s, &u)) return -1;
+        for (uint64_t i = 0; i < c.cap; ++i)
+            if (c.s[i].count != 0) c.s[i].count = counts_of(&u, c.s[i].x, c.s[i].y);
+        free(u.s);
+    }
 #define KEPT(i) (c.s[i].count != 0 && (keep ? keep[i] : c.s[i].count >= p->threshold))
     uint64_t ns = 0;
     for (uint64_t i = 0; i < c.cap; ++i)

@@ -48,9 +48,13 @@ typedef struct orc_result {
 void orc_project(double x, double y, double scale, int64_t* tx, int64_t* ty);
 /* cluster_sequential pipeline.hpp:92-126 (count-only mode, skip policy). */
 int orc_cluster(const double* xy, uint64_t n, const orc_params* p, orc_result* out);
-/* cluster_sequential with use_window_fix (window_fix agglomerate.hpp:212-246
- * in place of prune, pipeline.hpp:103). */
-int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int use_window_fix,
+/* cluster_sequential with options: ORC_WINDOW_FIX = use_window_fix
+ * (window_fix agglomerate.hpp:212-246 in place of prune, pipeline.hpp:103);
+ * ORC_DEDUPE = Mode::retain_points with dedupe_points (accumulator.hpp:165-169,
+ * 199-204): thresholds and counts on unique points per tile. */
+#define ORC_WINDOW_FIX 1
+#define ORC_DEDUPE 2
+int orc_cluster_ex(const double* xy, uint64_t n, const orc_params* p, int flags,
                    orc_result* out);
 /* agglomerate agglomerate.hpp:196-201 over caller tiles (any order). */
 int orc_agglomerate(const int64_t* tx, const int64_t* ty, const uint64_t* count, uint64_t n,

@@ -103,24 +103,31 @@ int ref_cluster(const double* xy, uint64_t n, const orc_params* p, unsigned work
     }
 }
 
-// cluster_sequential(pts, params, use_window_fix = true) pipeline.hpp:92-126
-// with the significant set of window_fix agglomerate.hpp:212-246.
-int ref_cluster_window_fix(const double* xy, uint64_t n, const orc_params* p, orc_result* out) {
+// cluster_sequential(pts, params, use_window_fix) pipeline.hpp:92-126 with
+// options: flags & 1 = use_window_fix (window_fix agglomerate.hpp:212-246),
+// flags & 2 = Mode::retain_points + dedupe_points.
+int ref_cluster_flags(const double* xy, uint64_t n, const orc_params* p, int flags,
+                      orc_result* out) {
     try {
         std::memset(out, 0, sizeof *out);
-        const raster::GridParams params = to_params(p);
+        raster::GridParams params = to_params(p);
+        const bool wf = flags & 1;
+        if (flags & 2) {
+            params.mode = raster::Mode::retain_points;
+            params.dedupe_points = true;
+        }
         std::span<const raster::Point> pts(reinterpret_cast<const raster::Point*>(xy), n);
         raster::TileAccumulator acc(params);
         acc.ingest(pts);
         out->n_ingested = acc.total_ingested();
         out->n_skipped = acc.skipped();
         out->n_distinct = acc.entry_count();
-        raster::SignificantTiles sig = raster::window_fix(acc, params);
+        raster::SignificantTiles sig = wf ? raster::window_fix(acc, params) : acc.prune();
         std::vector<std::pair<raster::Tile, std::uint64_t>> flat;
         flat.reserve(sig.size());
         for (const auto& [t, s] : sig) flat.emplace_back(t, s.count);
         std::sort(flat.begin(), flat.end());
-        raster::ClusterSet cs = raster::cluster_sequential(pts, params, true, nullptr);
+        raster::ClusterSet cs = raster::cluster_sequential(pts, params, wf, nullptr);
         return flatten(flat, cs, out);
     } catch (const std::exception& e) {
         g_err = e.what();
@@ -177,13 +184,14 @@ int ref_agglomerate(const int64_t* tx, const int64_t* ty, const uint64_t* count,
 // every retained point as (cluster id, x, y) in the reference's output order
 // (clusters by id, points sorted by point_less; write_cluster_points_csv
 // io.hpp:208-222). Returns the number of rows, or -1.
-int64_t ref_prime_points(const double* xy, uint64_t n, const orc_params* p, int64_t* cid,
-                         double* px, double* py, uint64_t cap) {
+int64_t ref_prime_points_ex(const double* xy, uint64_t n, const orc_params* p, int flags,
+                            int64_t* cid, double* px, double* py, uint64_t cap) {
     try {
         raster::GridParams params = to_params(p);
         params.mode = raster::Mode::retain_points;
+        params.dedupe_points = (flags & 2) != 0;
         std::span<const raster::Point> pts(reinterpret_cast<const raster::Point*>(xy), n);
-        raster::ClusterSet cs = raster::cluster_sequential(pts, params);
+        raster::ClusterSet cs = raster::cluster_sequential(pts, params, (flags & 1) != 0);
         uint64_t k = 0;
         for (const raster::Cluster& c : cs.clusters)
             for (const raster::Point& q : c.points) {
@@ -199,6 +207,11 @@ int64_t ref_prime_points(const double* xy, uint64_t n, const orc_params* p, int6
         g_err = e.what();
         return -1;
     }
+}
+
+int64_t ref_prime_points(const double* xy, uint64_t n, const orc_params* p, int64_t* cid,
+                         double* px, double* py, uint64_t cap) {
+    return ref_prime_points_ex(xy, n, p, 0, cid, px, py, cap);
 }
 
 // Strict policy check: index-free message of the first OOB point, as thrown

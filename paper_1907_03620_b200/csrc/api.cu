@@ -163,6 +163,11 @@ struct rg_ctx {
     u64* cp_off = nullptr;
     u64 cp_n = 0, cp_c = 0;
     bool cp_valid = false;
+    // dedupe_points (retain mode): point set + unique counts per tile
+    PtKey* ps = nullptr;
+    u64 ps_cap = 0, ps_used = 0;
+    Slot* ut = nullptr;
+    u64 ut_cap = 0;
     u8* wf_keep = nullptr;   // window_fix flags, one per table slot
     u64 wf_cap = 0;
 
@@ -289,10 +294,6 @@ rg_status validate(const rg_params* p, std::string& msg) {
         return RG_ERR_CONFIG;
     }
     // GPU-path limits.
-    if (p->dedupe_points) {
-        msg = "dedupe_points is not supported on the GPU path";
-        return RG_ERR_UNSUPPORTED;
-    }
     if (p->distance > 64) {
         msg = "distance > 64 is not supported on the GPU path";
         return RG_ERR_UNSUPPORTED;
@@ -393,6 +394,12 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
         CK(launch_table_clear(ctx->slots, ctx->cap, ctx->n_sm, ctx->st));
         ++ctx->launches;
     }
+    if (ctx->ps && ctx->ps_used) {
+        CK(cudaMemsetAsync(ctx->ps, 0xff, ctx->ps_cap * sizeof(PtKey), ctx->st));
+        CK(launch_table_clear(ctx->ut, ctx->ut_cap, ctx->n_sm, ctx->st));
+        ctx->launches += 1;
+    }
+    ctx->ps_used = 0;
     ctx->used = 0;
     ctx->table_dirty = false;
     ctx->state = rg_ctx::kAccum;
@@ -559,6 +566,76 @@ rg_status oob_error(rg_ctx* ctx, double x, double y) {
     return set_err(ctx, RG_ERR_OOB, "point (%f, %f) outside canvas bounds", x, y);
 }
 
+// ---- dedupe_points (retain mode): see dedupe.cu
+bool dedupe_active(const rg_ctx* ctx) {
+    return ctx->p.dedupe_points && ctx->p.mode == RG_MODE_RETAIN_POINTS;
+}
+
+PointSet point_set(const rg_ctx* c) { return PointSet{c->ps, c->ps_cap - 1}; }
+Table ut_table(const rg_ctx* c) { return make_table(c->ut, c->ut_cap, c->res.bits_y); }
+
+// The unique-count table follows the capacity of the count table (its keys
+// are a subset of the count table's).
+rg_status ensure_ut(rg_ctx* ctx) {
+    if (ctx->ut && ctx->ut_cap >= ctx->cap) return RG_OK;
+    Slot* nu = nullptr;
+    const u64 nc = std::max<u64>(ctx->cap, 1024);
+    rg_status s = alloc_table(ctx, nc, &nu);
+    if (s != RG_OK) return s;
+    if (ctx->ut) {
+        CK(launch_table_fold(ctx->ut, ctx->ut_cap, make_table(nu, nc, ctx->res.bits_y),
+                             ctx->scratch, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx->ut);
+    }
+    ctx->ut = nu;
+    ctx->ut_cap = nc;
+    return RG_OK;
+}
+
+// Point set at <= 50% load after `add` more distinct points.
+rg_status ensure_ps(rg_ctx* ctx, u64 add) {
+    const u64 need = ctx->ps_used + add;
+    if (ctx->ps && 2 * need <= ctx->ps_cap) return RG_OK;
+    const u64 nc = next_pow2(std::max<u64>(2 * need, 1024));
+    PtKey* np = nullptr;
+    CK(dalloc(&np, nc));
+    CK(cudaMemsetAsync(np, 0xff, nc * sizeof(PtKey), ctx->st));
+    if (ctx->ps) {
+        CK(launch_ps_rehash(ctx->ps, ctx->ps_cap, PointSet{np, nc - 1}, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        CK(cudaStreamSynchronize(ctx->st));
+        dfree(ctx->ps);
+    }
+    ctx->ps = np;
+    ctx->ps_cap = nc;
+    return RG_OK;
+}
+
+rg_status dedupe_ingest(rg_ctx* ctx, const double* dxy, u64 n) {
+    if (n == 0) return RG_OK;
+    rg_status s = ensure_ut(ctx);
+    if (s != RG_OK) return s;
+    s = ensure_ps(ctx, n);
+    if (s != RG_OK) return s;
+    CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(u64), ctx->st));
+    CK(launch_dedupe_ingest(dxy, n, ctx->grid, point_set(ctx), ut_table(ctx), ctx->scratch,
+                            ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    CK(cudaMemcpyAsync(&ctx->hctr->pad0[0], ctx->scratch, sizeof(u64), cudaMemcpyDeviceToHost,
+                       ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    ctx->ps_used += ctx->hctr->pad0[0];
+    return RG_OK;
+}
+
+rg_status ingest_counted(rg_ctx* ctx, const double* dxy, u64 n) {
+    rg_status s = ingest_device(ctx, dxy, n);
+    if (s == RG_OK && dedupe_active(ctx)) s = dedupe_ingest(ctx, dxy, n);
+    return s;
+}
+
 rg_status ingest_span(rg_ctx* ctx, const double* dxy, u64 n, bool* hit_oob, double* ox,
                       double* oy) {
     *hit_oob = false;
@@ -572,10 +649,10 @@ rg_status ingest_span(rg_ctx* ctx, const double* dxy, u64 n, bool* hit_oob, doub
             *hit_oob = true;
             *ox = pt[0];
             *oy = pt[1];
-            return ingest_device(ctx, dxy, f);
+            return ingest_counted(ctx, dxy, f);
         }
     }
-    return ingest_device(ctx, dxy, n);
+    return ingest_counted(ctx, dxy, n);
 }
 
 rg_status ingest_any(rg_ctx* ctx, const double* xy, u64 n, rg_memkind kind) {
@@ -696,6 +773,8 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
         if (window_fix) {
             if (ctx->wf_cap < ctx->cap) {
                 dfree(ctx->wf_keep);
+    dfree(ctx->ps);
+    dfree(ctx->ut);
     dfree(ctx->cp_xy);
     dfree(ctx->cp_off);
                 ctx->wf_cap = 0;
@@ -704,6 +783,12 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
             }
             CK(launch_window_mark(table_of(ctx), ctx->cap, ctx->p.threshold, ctx->grid.bits_x,
                                   ctx->wf_keep, ctx->n_sm, ctx->st));
+            ++ctx->launches;
+        }
+        if (dedupe_active(ctx) && ctx->ut) {
+            // threshold and reported counts follow the deduplicated counts
+            // (accumulator.hpp:165-169; window_fix decided on raw counts)
+            CK(launch_dedupe_counts(table_of(ctx), ctx->cap, ut_table(ctx), ctx->n_sm, ctx->st));
             ++ctx->launches;
         }
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
@@ -1061,6 +1146,8 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->part[1]);
     dfree(ctx->scratch);
     dfree(ctx->wf_keep);
+    dfree(ctx->ps);
+    dfree(ctx->ut);
     dfree(ctx->cp_xy);
     dfree(ctx->cp_off);
     dfree(ctx->sig_key);
@@ -1130,6 +1217,17 @@ static rg_status clone_into(rg_ctx* ctx, rg_ctx* src) {
                            cudaMemcpyDeviceToDevice, ctx->st));
         ctx->used = src->used;
     }
+    if (src->state == rg_ctx::kAccum && src->ps && src->ps_used) {
+        CK(dalloc(&ctx->ps, src->ps_cap));
+        CK(dalloc(&ctx->ut, src->ut_cap));
+        CK(cudaMemcpyAsync(ctx->ps, src->ps, src->ps_cap * sizeof(PtKey),
+                           cudaMemcpyDeviceToDevice, ctx->st));
+        CK(cudaMemcpyAsync(ctx->ut, src->ut, src->ut_cap * sizeof(Slot),
+                           cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->ps_cap = src->ps_cap;
+        ctx->ut_cap = src->ut_cap;
+        ctx->ps_used = src->ps_used;
+    }
     ctx->ingested = src->ingested;
     ctx->skipped = src->skipped;
     rg_status s = push_counters(ctx);
@@ -1191,6 +1289,21 @@ rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
         claimed = dst->hctr->pad0[0];
         dst->used += claimed;
     }
+    if (dedupe_active(dst) && src->ps && src->ps_used) {
+        // the merged point multiset is deduplicated as a whole at prune
+        s = ensure_ut(dst);
+        if (s != RG_OK) return s;
+        s = ensure_ps(dst, src->ps_used);
+        if (s != RG_OK) return s;
+        CK(cudaMemsetAsync(dst->scratch, 0, sizeof(u64), dst->st));
+        CK(launch_ps_fold(src->ps, src->ps_cap, dst->grid, point_set(dst), ut_table(dst),
+                          dst->scratch, dst->n_sm, dst->st));
+        ++dst->launches;
+        CK(cudaMemcpyAsync(&dst->hctr->pad0[0], dst->scratch, sizeof(u64),
+                           cudaMemcpyDeviceToHost, dst->st));
+        CK(cudaStreamSynchronize(dst->st));
+        dst->ps_used += dst->hctr->pad0[0];
+    }
     dst->ingested += src->ingested;
     dst->skipped += src->skipped;
     s = push_counters(dst);
@@ -1204,6 +1317,12 @@ rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
             ++c2->launches;
             if (e != cudaSuccess) return cuda_err(dst, e, "clear merged source");
         }
+        if (c2->ps && c2->ps_used) {
+            CK(cudaMemsetAsync(c2->ps, 0xff, c2->ps_cap * sizeof(PtKey), c2->st));
+            CK(launch_table_clear(c2->ut, c2->ut_cap, c2->n_sm, c2->st));
+            ++c2->launches;
+        }
+        c2->ps_used = 0;
         c2->used = c2->ingested = c2->skipped = 0;
         s = push_counters(c2);
         if (s != RG_OK) return set_err(dst, s, "%s", c2->err.c_str());
@@ -1252,6 +1371,9 @@ rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint6
 rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts,
                            uint64_t n, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;
+    if (dedupe_active(ctx))
+        return set_err(ctx, RG_ERR_UNSUPPORTED,
+                       "count pairs cannot be deduplicated (dedupe_points needs the points)");
     if (n && (!keys || !counts)) return set_err(ctx, RG_ERR_ARG, "null buffer");
     DevGuard guard(ctx->device);
     rg_status s = reopen_accumulator(ctx);

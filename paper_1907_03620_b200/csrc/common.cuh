@@ -48,6 +48,16 @@ struct __align__(16) Slot {
     u64 count;
 };
 
+// Point-set slot of the dedupe mode: the bit patterns of a canonical point
+// (never NaN, so {~0, ~0} marks an empty slot).
+struct __align__(16) PtKey {
+    u64 x, y;
+};
+struct PointSet {
+    PtKey* slots;
+    u64 mask;  // capacity - 1 (power of two)
+};
+
 // Projection + packing parameters (host computes scale = pow(10, p) with the
 // same libm as the reference, core.hpp:95; the device never calls pow).
 struct Grid {

@@ -116,6 +116,15 @@ cudaError_t launch_load_tiles(const long long* tx, const long long* ty, const u6
 cudaError_t launch_tile_extents(const long long* tx, const long long* ty, u64 n, long long* out,
                                 int n_sm, cudaStream_t st);
 
+// dedupe_points (dedupe.cu)
+cudaError_t launch_dedupe_ingest(const double* xy, u64 n, Grid g, PointSet ps, Table ut,
+                                 u64* n_new, int n_sm, cudaStream_t st);
+cudaError_t launch_ps_fold(const PtKey* src, u64 src_cap, Grid g, PointSet dst, Table ut,
+                           u64* n_new, int n_sm, cudaStream_t st);
+cudaError_t launch_ps_rehash(const PtKey* src, u64 src_cap, PointSet dst, int n_sm,
+                             cudaStream_t st);
+cudaError_t launch_dedupe_counts(Table t, u64 cap, Table ut, int n_sm, cudaStream_t st);
+
 // RASTER' cluster points (points.cu)
 struct PointsLaunch {
     const double* xy;

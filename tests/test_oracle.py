@@ -194,3 +194,37 @@ def test_window_fix_superset_and_live_reference():
             assert np.array_equal(r.tx, fixed.tx) and np.array_equal(r.ty, fixed.ty), trial
             assert np.array_equal(r.count, fixed.count), trial
             assert np.array_equal(r.cluster_id, fixed.cluster_id), trial
+
+
+def test_dedupe_kats(kat):
+    """test_accumulator.cpp:184-212 (raw multiset vs dedupe_points)."""
+    for c in kat["dedupe"]:
+        gp = GridParams(precision=c["precision"], threshold=c["threshold"], min_cluster_size=1)
+        r = O.port_cluster(np.array(c["points"]), gp, dedupe=c["dedupe"])
+        assert r.tx.tolist() == [c["tile"][0]] and r.ty.tolist() == [c["tile"][1]], c["cite"]
+        assert r.count.tolist() == [c["count"]], c["cite"]
+        if O.ref() is not None:
+            cid, px, py = O.ref_prime_points(np.array(c["points"]), gp, dedupe=c["dedupe"])
+            assert len(px) == c["n_points"], c["cite"]
+
+
+def test_dedupe_vs_live_reference():
+    """Random inputs with heavy duplication, signed zeros and both
+    significance paths, against the reference compiled here."""
+    if O.ref() is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(7)
+    for trial in range(8):
+        gp = GridParams(precision=2, threshold=int(rng.integers(2, 6)),
+                        min_cluster_size=int(rng.integers(1, 4)))
+        base = np.round(rng.normal(0, 0.05, size=(3000, 2)), 3)
+        pts = base[rng.integers(0, len(base), 9000)]
+        pts[:50] *= -0.0  # signed zeros: (-0.0, -0.0) == (0.0, 0.0)
+        wf = bool(trial % 2)
+        mine = O.port_cluster(pts, gp, window_fix=wf, dedupe=True)
+        ref = O.ref_cluster_flags(pts, gp, window_fix=wf, dedupe=True)
+        assert np.array_equal(mine.tx, ref.tx) and np.array_equal(mine.ty, ref.ty), trial
+        assert np.array_equal(mine.count, ref.count), trial
+        assert np.array_equal(mine.cluster_id, ref.cluster_id), trial
+        plain = O.port_cluster(pts, gp, window_fix=wf)
+        assert mine.tx.size <= plain.tx.size
