@@ -773,10 +773,6 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
         if (window_fix) {
             if (ctx->wf_cap < ctx->cap) {
                 dfree(ctx->wf_keep);
-    dfree(ctx->ps);
-    dfree(ctx->ut);
-    dfree(ctx->cp_xy);
-    dfree(ctx->cp_off);
                 ctx->wf_cap = 0;
                 CK(dalloc(&ctx->wf_keep, ctx->cap));
                 ctx->wf_cap = ctx->cap;
