@@ -176,6 +176,22 @@ __device__ __forceinline__ bool table_add(const Table& t, u64 key, u64 cnt) {
     }
 }
 
+// table_add for keys that are usually new (K1's evictions): the claim is
+// attempted first, so a new key costs one L2 round trip (the CAS) instead of
+// a load followed by the CAS; an existing key costs the CAS's read of it.
+__device__ __forceinline__ bool table_add_cas(const Table& t, u64 key, u64 cnt) {
+    Probe p(key, t);
+    while (true) {
+        Slot* s = t.slots + p.slot();
+        const u64 old = atomicCAS(&s->key, kEmpty, key);
+        if (old == kEmpty || old == key) {
+            red_add(&s->count, cnt);
+            return old == kEmpty;
+        }
+        p.next(t);
+    }
+}
+
 // Lookup: returns the slot's value word, or kEmpty when the key is absent.
 // TileCounts::count_of accumulator.hpp:53-61.
 __device__ __forceinline__ u64 table_find(const Table& t, u64 key) {

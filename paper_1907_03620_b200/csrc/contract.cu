@@ -61,169 +61,236 @@ struct K1Params {
     u32 budget;  // per-warp bound on (claimed keys + cached entries)
 };
 
-// Cache slot of a tile: direct-mapped by position in an 8 x 16-tile window
-// (low 3 column bits, low 4 row bits), so the tiles of one cluster (a few
-// tiles across) never evict each other; keys of unrelated regions are spread
-// by their low coordinate bits.
-#ifndef RG_CACHE_HASH
-__device__ __forceinline__ u32 cache_slot(u64 key, u32 bits_y) {
-    return (((u32)(key >> bits_y) & 7u) << 4) | ((u32)key & 15u);
-}
-#else
-__device__ __forceinline__ u32 cache_slot(u64 key, u32) {
-    return (((u32)key ^ (u32)(key >> 32) * 0x85EBCA6Bu) * 0x9E3779B1u) >> 25;
-}
-#endif
-
-// Projection + packing; kNarrow when every canvas column/row index fits in
-// int32 (the host checks), so floor+convert is one cvt.rmi.s32.f64 and the
-// origin shift is 32-bit. Identical results to pack_key for such canvases.
+// Cache keys. In the narrow case (every canvas column/row index fits int32,
+// checked on the host) the per-warp cache works on the unpacked pair
+// (kx << 32 | ky): building it costs no shift, its slot is two bit
+// operations, and the table's packed key (kx << bits_y | ky) is formed only
+// when an entry leaves the cache. Otherwise the packed key is used
+// throughout. Out-of-bounds points get kEmpty (a valid pair has kx < 2^31).
 template <bool kNarrow>
-__device__ __forceinline__ u64 key_of(const Grid& g, double x, double y) {
-    if (kNarrow) {
+struct KeyOps;
+
+template <>
+struct KeyOps<true> {
+    __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
         const int tx = __double2int_rd(__dmul_rn(x, g.scale));
         const int ty = __double2int_rd(__dmul_rn(y, g.scale));
         const u32 kx = (u32)(tx - (int)g.origin_x);
         const u32 ky = (u32)(ty - (int)g.origin_y);
-        return ((u64)kx << g.bits_y) | ky;
-    } else {
-        return pack_key(g, x, y);
+        return in_bounds(g, x, y) ? (((u64)kx << 32) | ky) : kEmpty;
     }
-}
-
-struct Rows {
-    double x[kBatch], y[kBatch];
+    // Direct-mapped by position in an 8 x 16-tile window (low 3 column bits,
+    // low 4 row bits): the few tiles of one cluster never evict each other.
+    __device__ static __forceinline__ u32 slot(u64 ck, u32) {
+        return (((u32)(ck >> 32) & 7u) << 4) | ((u32)ck & 15u);
+    }
+    __device__ static __forceinline__ u64 table_key(u64 ck, u32 bits_y) {
+        return ck == kEmpty ? kEmpty : (((ck >> 32) << bits_y) | (u32)ck);
+    }
 };
 
-// Loads the lane's point of the kBatch rows starting at point index p0
-// (p0 = first point of the batch; `left` = valid points in the batch, <=
-// 32*kBatch). Missing points become NaN, which fails the bounds test.
-template <bool kAligned>
-__device__ __forceinline__ void load_rows(const double* xy, u64 p0, u32 left, int lane, u64 pol,
-                                          Rows& o) {
-    if (kAligned && left == 32 * kBatch) {
-        // Full batch (all but a segment's last batch): one base pointer,
-        // immediate offsets, no per-row predicates.
-        const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
-#pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            const double2 v = ld_point_stream(base + b * 32, pol);
-            o.x[b] = v.x;
-            o.y[b] = v.y;
-        }
-        return;
+template <>
+struct KeyOps<false> {
+    __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
+        const u64 k = pack_key(g, x, y);
+        return in_bounds(g, x, y) ? k : kEmpty;
     }
-#pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-        if ((u32)(b * 32 + lane) < left) {
-            if (kAligned) {
-                const double2 v =
-                    ld_point_stream(reinterpret_cast<const double2*>(xy) + p0 + b * 32 + lane, pol);
-                o.x[b] = v.x;
-                o.y[b] = v.y;
-            } else {
-                const double* q = xy + 2 * (p0 + b * 32 + lane);
-                o.x[b] = q[0];
-                o.y[b] = q[1];
-            }
-        } else {
-            o.x[b] = o.y[b] = __longlong_as_double(0x7ff8000000000000ll);
-        }
+    __device__ static __forceinline__ u32 slot(u64 k, u32 bits_y) {
+        return (((u32)(k >> bits_y) & 7u) << 4) | ((u32)k & 15u);
     }
+    __device__ static __forceinline__ u64 table_key(u64 k, u32) { return k; }
+};
+
+__device__ __forceinline__ u32 match_any64(u64 v) {
+    u32 m;
+    asm volatile("match.any.sync.b64 %0, %1, 0xffffffff;" : "=r"(m) : "l"(v));
+    return m;
+}
+
+__device__ __forceinline__ u32 ballot(bool p) {
+    u32 m;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n vote.sync.ballot.b32 %0, q, 0xffffffff;\n}"
+        : "=r"(m)
+        : "r"((u32)p));
+    return m;
 }
 
 // Per-warp shared state of K1.
+#ifdef RG_K1_MATCH
+typedef u64 CacheCount;
+#else
+typedef u32 CacheCount;  // bounded by the per-segment overflow check in k_contract
+#endif
+
 struct WarpSmem {
-    u64 ckey[kCacheSlots];   // direct-mapped write-back cache: keys
-    u64 ccnt[kCacheSlots];   //                                 counts
-    u64 skey[64];            // staged (key, count) pairs bound for the HBM table
+    u64 ckey[kCacheSlots];          // direct-mapped write-back cache: cache keys
+    CacheCount ccnt[kCacheSlots];   //                                 counts
+    u64 skey[64];            // staged (table key, count) pairs bound for the HBM table
     u64 scnt[64];
     unsigned char owner[kCacheSlots];
 };
 
 struct K1State {
-    u32 pot;      // warp-uniform: claimed keys + occupied cache entries + staged entries
-    u32 slen;     // warp-uniform: staged entries
+    u32 pot;      // warp-uniform: bound on claimed keys + cache entries + staged entries
+    u32 slen;     // warp-uniform: staged entries (some may be placeholders)
     u32 claims;   // per lane: keys this lane claimed in the table
     u64 added;    // per lane: points this lane added to the table (= ingested, by conservation)
 };
 
 // Flush the staging list with every lane active: one table_add per entry,
 // lanes in parallel (the divergent, latency-bound part of a miss is paid
-// once per 32 misses instead of once per row).
+// once per 32 misses instead of once per row). Placeholder entries (a miss
+// that filled an empty cache slot reserved one) carry kEmpty and are skipped.
 __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State& s, int lane) {
-    u32 c = 0;
+    u32 c = 0, ph = 0;
     for (u32 e = lane; e < s.slen; e += 32) {
-        c += table_add(t, w.skey[e], w.scnt[e]) ? 1u : 0u;
-        s.added += w.scnt[e];
+        const u64 k = w.skey[e];
+        if (k != kEmpty) {
+#ifdef RG_K1_NOFLUSH  // experiment: drop evictions (results are wrong)
+            c += (w.scnt[e] == 12345) ? 1u : 0u;
+#else
+            c += table_add_cas(t, k, w.scnt[e]) ? 1u : 0u;
+#endif
+            s.added += w.scnt[e];
+        } else {
+            ++ph;
+        }
     }
-    const u32 claimed = __reduce_add_sync(kFull, c);
+    // (claimed keys) | (placeholders << 16); slen <= 64
+    const u32 r = __reduce_add_sync(kFull, c | (ph << 16));
     s.claims += c;
-    s.pot = s.pot - s.slen + claimed;
+    // a placeholder's cache entry stays in the cache: it keeps its unit
+    s.pot = s.pot - (s.slen - (r >> 16)) + (r & 0xffffu);
     s.slen = 0;
     __syncwarp();
 }
 
-// One batch of kBatch rows already in registers.
+#ifndef RG_K1_MATCH
+// One batch of kBatch rows already in registers (one point per lane per
+// row). Every lane looks its tile up in the per-warp cache; a hit adds 1
+// with a shared-memory reduction (fire-and-forget: the warp does not wait,
+// and lanes of one tile serialise inside the shared-memory atomic unit
+// instead of in a match/leader/add chain). Misses are resolved per slot:
+// one missing lane wins the slot, evicts the old occupant into the staging
+// list (or leaves a placeholder if the slot was empty) and installs its key
+// with count 0; then every missing lane whose key now owns its slot adds
+// 1, and the others (a different key won the slot in this row) stage
+// (key, 1) themselves.
 template <bool kNarrow>
-__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const Rows& cur,
-                                              WarpSmem& w, K1State& s, int lane, u32 lane_bit,
-                                              u32 lt_mask) {
+__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const double* x,
+                                              const double* y, WarpSmem& w, K1State& s,
+                                              int lane, u32 lt_mask) {
+    using K = KeyOps<kNarrow>;
     u64 key[kBatch];
-    bool inb[kBatch];
+    u32 cs[kBatch];
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-        inb[b] = in_bounds(g, cur.x[b], cur.y[b]);
-        // Computed unconditionally (no branch): for out-of-bounds or NaN
-        // lanes the conversion result is meaningless and replaced by EMPTY.
-        const u64 k = key_of<kNarrow>(g, cur.x[b], cur.y[b]);
-        key[b] = inb[b] ? k : kEmpty;
+        key[b] = K::cache_key(g, x[b], y[b]);
+        cs[b] = K::slot(key[b], g.bits_y);
     }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+        const bool valid = key[b] != kEmpty;
+        const bool hit = valid && w.ckey[cs[b]] == key[b];
+        if (hit) atomicAdd(&w.ccnt[cs[b]], 1u);
+        const bool miss = valid && !hit;
+        const u32 missmask = ballot(miss);
+        if (missmask) {
+            if (miss) w.owner[cs[b]] = (unsigned char)lane;
+            __syncwarp();
+            const bool win = miss && w.owner[cs[b]] == lane;
+            u64 sk = kEmpty, sc = 0;
+            if (win) {
+                sk = K::table_key(w.ckey[cs[b]], g.bits_y);  // kEmpty: placeholder
+                sc = w.ccnt[cs[b]];
+                w.ckey[cs[b]] = key[b];
+                w.ccnt[cs[b]] = 0;
+            }
+            __syncwarp();
+            bool lose = false;
+            if (miss) {
+                if (w.ckey[cs[b]] == key[b]) {
+                    atomicAdd(&w.ccnt[cs[b]], 1u);
+                } else {
+                    lose = true;
+                    sk = K::table_key(key[b], g.bits_y);
+                    sc = 1;
+                }
+            }
+            // each winner and each loser adds one to (cache + staged entries)
+            const u32 smask = ballot(win || lose);
+            if (win || lose) {
+                const u32 pos = s.slen + __popc(smask & lt_mask);
+                w.skey[pos] = sk;
+                w.scnt[pos] = sc;
+            }
+            const u32 ns = __popc(smask);
+            s.slen += ns;
+            s.pot += ns;
+            __syncwarp();
+            if (s.slen > 64 - 32) flush_stage(t, w, s, lane);
+        }
+    }
+}
+#else
+// One batch of kBatch rows already in registers (one point per lane per
+// row). Keys and match masks of all rows are formed first so their
+// latencies overlap; rows are then merged into the cache in order (a later
+// row's hit must see an earlier row's install).
+template <bool kNarrow>
+__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const double* x,
+                                              const double* y, WarpSmem& w, K1State& s,
+                                              int lane, u32 lt_mask) {
+    using K = KeyOps<kNarrow>;
+    u64 key[kBatch];
     u32 peers[kBatch];
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) peers[b] = __match_any_sync(kFull, key[b]);
+    for (int b = 0; b < kBatch; ++b) key[b] = K::cache_key(g, x[b], y[b]);
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) peers[b] = match_any64(key[b]);
 #pragma unroll
     for (int b = 0; b < kBatch; ++b) {
-        const bool leader = inb[b] && ((peers[b] & (0u - peers[b])) == lane_bit);
-        const u32 cs = cache_slot(key[b], g.bits_y);
-        const u64 cnt = __popc(peers[b]);
+        // the group's lowest lane leads; out-of-bounds lanes never do
+        const bool leader = key[b] != kEmpty && (peers[b] & lt_mask) == 0;
+        const u32 cs = K::slot(key[b], g.bits_y);
+        const u32 cnt = __popc(peers[b]);
         // Hit: the slot holds this key. Distinct keys never hit the same
         // slot, so hitting leaders add without arbitration.
         const bool hit = leader && w.ckey[cs] == key[b];
         if (hit) w.ccnt[cs] += cnt;
         const bool miss = leader && !hit;
-        const u32 missmask = __ballot_sync(kFull, miss);
+        const u32 missmask = ballot(miss);
         if (missmask) {
-            // One missing leader per slot installs its key; the slot's old
-            // occupant (if any) and the other missing leaders are staged.
+            // One missing leader per slot installs its key; every missing
+            // leader reserves a staging entry for what it displaces: the
+            // slot's old occupant (winner) or its own group (losers). A
+            // winner that found the slot empty leaves a placeholder. Each
+            // miss therefore adds one to (cache entries + staged entries).
             if (miss) w.owner[cs] = (unsigned char)lane;
             __syncwarp();
-            const bool win = miss && w.owner[cs] == lane;
-            u64 sk = key[b], sc = cnt;
-            bool was_empty = false;
-            if (win) {
-                sk = w.ckey[cs];
-                sc = w.ccnt[cs];
-                was_empty = sk == kEmpty;
-                w.ckey[cs] = key[b];
-                w.ccnt[cs] = cnt;
-            }
-            const bool stage = miss && !was_empty;
-            const u32 smask = __ballot_sync(kFull, stage);
-            const u32 emask = __ballot_sync(kFull, was_empty);
-            if (stage) {
-                const u32 pos = s.slen + __popc(smask & lt_mask);
+            if (miss) {
+                u64 sk = K::table_key(key[b], g.bits_y), sc = cnt;
+                if (w.owner[cs] == lane) {
+                    sk = K::table_key(w.ckey[cs], g.bits_y);
+                    sc = w.ccnt[cs];
+                    w.ckey[cs] = key[b];
+                    w.ccnt[cs] = cnt;
+                }
+                const u32 pos = s.slen + __popc(missmask & lt_mask);
                 w.skey[pos] = sk;
                 w.scnt[pos] = sc;
             }
-            s.slen += __popc(smask);
-            s.pot += __popc(smask) + __popc(emask);
+            const u32 nm = __popc(missmask);
+            s.slen += nm;
+            s.pot += nm;
             __syncwarp();
-            if (s.slen >= 32) flush_stage(t, w, s, lane);
+            if (s.slen > 64 - 32) flush_stage(t, w, s, lane);
         }
-        __syncwarp();
     }
 }
+
+#endif  // RG_K1_MATCH
 
 // Asynchronous 16-byte global->shared copy (LDGSTS), L1-bypassing, with an
 // L2 evict-first policy: the points are read exactly once.
@@ -244,17 +311,75 @@ __device__ __forceinline__ void cp_async_wait() {
 #endif
 constexpr int kRing = RG_K1_RING;  // rows in flight per warp (multiple of kBatch)
 
+// One segment of nr rows starting at `base` (this lane's point of the first
+// row). kFullRows: every point of every row exists (all segments but
+// possibly the last), so loads need no per-lane checks. `valid` = points of
+// the segment (only read when !kFullRows). Each lane copies its own point
+// into its own ring column, so no cross-lane synchronisation is needed
+// around the ring. Returns the row index at which the warp ran out of
+// budget, or nr.
+template <bool kAligned, bool kNarrow, bool kFullRows>
+__device__ __forceinline__ u32 run_segment(const double2* base, const double* xy_base, u32 nr,
+                                           u32 valid, double2 (*ring)[32], const Grid& g,
+                                           const Table& t, WarpSmem& w, K1State& st, int lane,
+                                           u32 lt_mask, u64 pol, u32 budget) {
+    auto issue = [&](u32 row) {
+        if (row < nr) {
+            const u32 idx = row * 32 + lane;
+            if (kFullRows || idx < valid) {
+                double2* dst = &ring[row % kRing][lane];
+                if (kAligned) {
+                    cp_async16(dst, base + row * 32, pol);
+                } else {
+                    dst->x = xy_base[2 * (u64)idx];
+                    dst->y = xy_base[2 * (u64)idx + 1];
+                }
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < kRing; ++k) issue(k);
+    for (u32 j = 0; j < nr; j += kBatch) {
+        cp_async_wait<kRing - kBatch>();
+        double x[kBatch], y[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const u32 row = j + b;
+            if (kFullRows || (row < nr && row * 32 + lane < valid)) {
+                const double2 v = ring[row % kRing][lane];
+                x[b] = v.x;
+                y[b] = v.y;
+            } else {
+                x[b] = y[b] = __longlong_as_double(0x7ff8000000000000ll);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) issue(j + kRing + b);
+#ifdef RG_K1_STREAM_ONLY  // experiment: the load path alone (results are wrong)
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) st.added += (x[b] + y[b] > 1e300) ? 1 : 0;
+#else
+        process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask);
+#endif
+        if (st.pot >= budget) return j + kBatch < nr ? j + kBatch : nr;
+    }
+    return nr;
+}
+
 template <bool kAligned, bool kNarrow>
 __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ WarpSmem s_warp[kWarpsPerBlock];
     __shared__ __align__(16) double2 s_ring[kWarpsPerBlock][kRing][32];
 
     const int lane = threadIdx.x & 31;
-    const u32 lane_bit = 1u << lane;
-    const u32 lt_mask = lane_bit - 1;
+    const u32 lt_mask = (1u << lane) - 1;
     WarpSmem& w = s_warp[threadIdx.x >> 5];
     double2 (*ring)[32] = s_ring[threadIdx.x >> 5];
-    for (int i = lane; i < kCacheSlots; i += 32) w.ckey[i] = kEmpty;
+    for (int i = lane; i < kCacheSlots; i += 32) {
+        w.ckey[i] = kEmpty;
+        w.ccnt[i] = 0;
+    }
     __syncwarp();
 
     const Grid g = P.g;
@@ -300,21 +425,6 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
             P.partial_out[at].next_row = row;
         }
     };
-    // Issue the copy of row `row` (if it exists) into its ring slot; one
-    // commit group per row on every lane keeps the group count uniform.
-    auto issue = [&](u64 row, u64 row_end, u64 row0) {
-        const u64 idx = row * 32 + lane;
-        if (row < row_end && idx < P.n) {
-            double2* dst = &ring[(row - row0) % kRing][lane];
-            if (kAligned) {
-                cp_async16(dst, pts + idx, pol);
-            } else {
-                dst->x = P.xy[2 * idx];
-                dst->y = P.xy[2 * idx + 1];
-            }
-        }
-        cp_async_commit();
-    };
 
     u64 seg, row0;
     bool from_ticket;
@@ -323,53 +433,56 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         const u64 row_end = min((seg + 1) * P.rows_per_seg, P.n_rows);
         if (lane == 0 && (from_ticket || P.n_partial_in == 0))
             pending = atomicAdd(&P.ctr->ticket, 1ull);
-#pragma unroll
-        for (int k = 0; k < kRing; ++k) issue(row0 + k, row_end, row0);
-        for (u64 r = row0; r < row_end; r += kBatch) {
-            // rows r .. r+kBatch-1 have landed once at most kRing-kBatch
-            // younger groups are pending
-            cp_async_wait<kRing - kBatch>();
-            Rows cur;
-            u32 left = 0;
-#pragma unroll
-            for (int b = 0; b < kBatch; ++b) {
-                const u64 row = r + b;
-                const u64 idx = row * 32 + lane;
-                if (row < row_end && idx < P.n) {
-                    const double2 v = ring[(row - row0) % kRing][lane];
-                    cur.x[b] = v.x;
-                    cur.y[b] = v.y;
-                } else {
-                    cur.x[b] = cur.y[b] = __longlong_as_double(0x7ff8000000000000ll);
+#ifndef RG_K1_MATCH
+        // 32-bit cache counts: a segment adds at most 32 * rows_per_seg
+        // (<= 8192) to an entry, so moving large counts out here keeps
+        // every entry below 2^31 + 8192.
+        {
+            u32 gc = 0;
+            for (int i = lane; i < kCacheSlots; i += 32) {
+                if (w.ccnt[i] >= 0x80000000u) {
+                    const u64 k = KeyOps<kNarrow>::table_key(w.ckey[i], g.bits_y);
+                    gc += table_add_cas(t, k, w.ccnt[i]) ? 1u : 0u;
+                    st.added += w.ccnt[i];
+                    w.ccnt[i] = 0;
                 }
-                if (row < row_end) left += (u32)min(P.n - row * 32, (u64)32);
             }
-#pragma unroll
-            for (int b = 0; b < kBatch; ++b) issue(r + kRing + b, row_end, row0);
-            n_valid += left;
-            process_batch<kNarrow>(g, t, cur, w, st, lane, lane_bit, lt_mask);
-            if (st.pot >= P.budget) {
-                if (r + kBatch < row_end) record_partial(seg, r + kBatch);
-                stopped = true;
-                break;
-            }
+            st.claims += gc;
+            st.pot += __reduce_add_sync(kFull, gc);  // the entry stays cached too
+            __syncwarp();
         }
-        if (stopped) {
+#endif
+        const u32 nr = (u32)(row_end - row0);
+        const u64 p0 = row0 * 32;
+        const u32 valid = (u32)min(P.n - p0, (u64)nr * 32);
+        const double2* base = pts + p0 + lane;
+        const double* xy_base = P.xy + 2 * p0;
+        u32 done;
+        if (valid == nr * 32 && nr % kBatch == 0)
+            done = run_segment<kAligned, kNarrow, true>(base, xy_base, nr, valid, ring, g, t, w,
+                                                        st, lane, lt_mask, pol, P.budget);
+        else
+            done = run_segment<kAligned, kNarrow, false>(base, xy_base, nr, valid, ring, g, t, w,
+                                                         st, lane, lt_mask, pol, P.budget);
+        cp_async_wait<0>();
+        n_valid += min((u64)done * 32, (u64)valid);
+        if (done < nr || st.pot >= P.budget) {
+            if (done < nr) record_partial(seg, row0 + done);
             // hand back the prefetched ticket too
             const u64 tk = __shfl_sync(kFull, pending, 0);
             if (tk != ~0ull && tk < P.n_seg) record_partial(tk, tk * P.rows_per_seg);
+            stopped = true;
             break;
         }
         have = fetch(seg, row0, from_ticket);
     }
-    cp_async_wait<0>();
 
     // Write back staged entries and the cache.
     flush_stage(t, w, st, lane);
     for (int i = lane; i < kCacheSlots; i += 32) {
-        const u64 k = w.ckey[i];
+        const u64 k = KeyOps<kNarrow>::table_key(w.ckey[i], g.bits_y);
         if (k != kEmpty) {
-            st.claims += table_add(t, k, w.ccnt[i]) ? 1u : 0u;
+            st.claims += table_add_cas(t, k, w.ccnt[i]) ? 1u : 0u;
             st.added += w.ccnt[i];
         }
     }
