@@ -204,12 +204,19 @@ __global__ void __launch_bounds__(256) k_sorted_union(const u64* skey, const u64
 // (x+1,y)). Window-local components are found by min-label propagation with
 // pointer jumping in shared memory (converges in a few rounds; labels only
 // decrease), then every tile is linked to its component's smallest member.
+// The block's 256 keys plus the next kC1Extra (where the next column of
+// the window's last tiles usually lies) are staged in shared memory, so the
+// neighbour searches run on shared memory; a search that leaves the staged
+// range continues in global memory.
+constexpr u32 kC1Extra = 256;
+
 __global__ void __launch_bounds__(256) k_sorted_union_c1(const u64* skey, const u64* n_sig_p,
                                                          u32 bits_y, u32* parent, u32* size,
                                                          u64* npts, SortedEdges el) {
     __shared__ u32 s_lbl[256];
     __shared__ u32 s_wcnt[8];
     __shared__ u64 s_base;
+    __shared__ u64 s_key[256 + kC1Extra];
     const u64 n = *n_sig_p;
     const u32 loc = threadIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -219,18 +226,42 @@ __global__ void __launch_bounds__(256) k_sorted_union_c1(const u64* skey, const 
         const u64 base = i - loc;
         const u64 wend = base + 256;
         const bool valid = i < n;
+        const u32 staged = (u32)min((u64)(256 + kC1Extra), n - base);
+        for (u32 q = loc; q < 256 + kC1Extra; q += 256) s_key[q] = q < staged ? skey[base + q] : ~0ull;
+        __syncthreads();
+        // key at global index j (staged range from shared memory)
+        auto key_at = [&](u64 j) -> u64 { return j - base < staged ? s_key[j - base] : skey[j]; };
         u32 nb[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
         if (valid) {
-            const u64 k = skey[i];
+            const u64 k = s_key[loc];
             const u64 y = k & ymask;
-            if (i + 1 < n && skey[i + 1] == k + 1) nb[0] = (u32)(i + 1);  // (x, y+1)
+            if (i + 1 < n && key_at(i + 1) == k + 1) nb[0] = (u32)(i + 1);  // (x, y+1)
             const u64 nxk = k + (1ull << bits_y);                          // (x+1, y)
             if ((nxk >> bits_y) == (k >> bits_y) + 1) {
                 const u64 lo = y > 0 ? nxk - 1 : nxk;
-                u64 j = gallop(skey, n, i + 1, lo);
+                u64 j;
+                if (s_key[staged - 1] >= lo) {
+                    // first staged index > loc with key >= lo: gallop, then bisect
+                    u32 a = loc + 1, step = 1, b = loc + 1;
+                    while (b < staged && s_key[b] < lo) {
+                        a = b;
+                        b += step;
+                        step <<= 1;
+                    }
+                    if (b > staged) b = staged;
+                    while (a < b) {
+                        const u32 m = (a + b) >> 1;
+                        if (s_key[m] < lo) a = m + 1;
+                        else b = m;
+                    }
+                    j = base + a;
+                } else {
+                    j = gallop(skey, n, base + staged, lo);
+                }
                 u32 dm = 0xffffffffu, d0 = 0xffffffffu, dp = 0xffffffffu;
-                for (; j < n && skey[j] <= nxk + 1 && (y < ymask || skey[j] <= nxk); ++j) {
-                    const u64 kj = skey[j];
+                for (; j < n; ++j) {
+                    const u64 kj = key_at(j);
+                    if (kj > nxk + 1 || (y == ymask && kj > nxk)) break;
                     if (kj == nxk - 1 && y > 0) dm = (u32)j;
                     else if (kj == nxk) d0 = (u32)j;
                     else if (kj == nxk + 1) dp = (u32)j;
@@ -396,7 +427,10 @@ __global__ void k_sorted_label(const u32* parent, const u32* flag, const u32* sc
 // counting sort on the column (histogram, scan, scatter), then a segmented
 // sort of each column by row — two passes over the data instead of the
 // radix sort's five, and columns are short (tens of tiles).
-constexpr u32 kColBitsMax = 22;
+#ifndef RG_COL_BITS_MAX
+#define RG_COL_BITS_MAX 22
+#endif
+constexpr u32 kColBitsMax = RG_COL_BITS_MAX;
 
 __global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt, u32* max_col) {
     // Consecutive tiles (bucket order) share columns: one atomic per column

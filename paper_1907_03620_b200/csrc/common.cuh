@@ -88,6 +88,7 @@ struct Table {
 struct Probe {
     u64 b0, b;
     u32 pos;
+    Probe() = default;
     __device__ __forceinline__ Probe(u64 key, const Table& t) {
         const u64 ky = key & ((1ull << t.bits_y) - 1);
         const u64 block =

@@ -117,6 +117,13 @@ __device__ __forceinline__ u32 ballot(bool p) {
 }
 
 // Per-warp shared state of K1.
+// Staging list: flushed once more than kStageCap - 32 entries wait (a row
+// adds at most 32).
+#ifndef RG_K1_STAGE
+#define RG_K1_STAGE 64
+#endif
+constexpr u32 kStageCap = RG_K1_STAGE;
+
 #ifdef RG_K1_MATCH
 typedef u64 CacheCount;
 #else
@@ -126,8 +133,8 @@ typedef u32 CacheCount;  // bounded by the per-segment overflow check in k_contr
 struct WarpSmem {
     u64 ckey[kCacheSlots];          // direct-mapped write-back cache: cache keys
     CacheCount ccnt[kCacheSlots];   //                                 counts
-    u64 skey[64];            // staged (table key, count) pairs bound for the HBM table
-    u64 scnt[64];
+    u64 skey[kStageCap];     // staged (table key, count) pairs bound for the HBM table
+    u64 scnt[kStageCap];
     unsigned char owner[kCacheSlots];
 };
 
@@ -157,7 +164,7 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
             ++ph;
         }
     }
-    // (claimed keys) | (placeholders << 16); slen <= 64
+    // (claimed keys) | (placeholders << 16); slen <= kStageCap
     const u32 r = __reduce_add_sync(kFull, c | (ph << 16));
     s.claims += c;
     // a placeholder's cache entry stays in the cache: it keeps its unit
@@ -229,7 +236,7 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
             s.slen += ns;
             s.pot += ns;
             __syncwarp();
-            if (s.slen > 64 - 32) flush_stage(t, w, s, lane);
+            if (s.slen > kStageCap - 32) flush_stage(t, w, s, lane);
         }
     }
 }
@@ -285,7 +292,7 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
             s.slen += nm;
             s.pot += nm;
             __syncwarp();
-            if (s.slen > 64 - 32) flush_stage(t, w, s, lane);
+            if (s.slen > kStageCap - 32) flush_stage(t, w, s, lane);
         }
     }
 }
@@ -633,7 +640,10 @@ __global__ void k_first_oob(const double* xy, u64 n, Grid g, u64* first) {
 // >= 256 staged entries it reserves output space with one atomic and writes
 // them out contiguously (the slots are re-read from L1/L2). Waiting on the
 // reservation is paid once per 256 outputs instead of once per step.
-constexpr int kK2Items = 8;
+#ifndef RG_K2_ITEMS
+#define RG_K2_ITEMS 4
+#endif
+constexpr int kK2Items = RG_K2_ITEMS;
 constexpr int kK2Stage = 256 + 32 * kK2Items;
 
 struct K2Out {
@@ -659,8 +669,8 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
         const u64 pos = at + e;
         o.sig_key[pos] = k;
         o.sig_cnt[pos] = v;
-        o.parent[pos] = (u32)pos;
         if (o.size) {  // hash-probe K3 only (the sorted K3 initialises its own)
+            o.parent[pos] = (u32)pos;
             o.size[pos] = 0;
             o.npts[pos] = 0;
             o.min_key[pos] = kEmpty;
@@ -837,9 +847,13 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
                            Counters* ctr, int n_sm, cudaStream_t st) {
+#ifndef RG_K2_BPS
+#define RG_K2_BPS 16
+#endif
     const u64 per_block = 256ull * kK2Items;
     const u64 want = (cap + per_block - 1) / per_block;
-    const int blocks = (int)(want < (u64)n_sm * 16 ? (want ? want : 1) : (u64)n_sm * 16);
+    const u64 mx = (u64)n_sm * RG_K2_BPS;
+    const int blocks = (int)(want < mx ? (want ? want : 1) : mx);
     const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid};
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, keep, o, ctr);
     return cudaGetLastError();
