@@ -4,6 +4,7 @@
 // staging, and small utility kernels. No CPU fallback anywhere: every
 // computational entry point runs on the device or fails.
 #include <algorithm>
+#include <cstddef>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -150,6 +151,7 @@ struct rg_ctx {
     int max_warps = 0;
     cudaStream_t own = nullptr, st = nullptr, copy_st = nullptr;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaEvent_t ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;  // fused prune + agglomerate
     cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
 
     Slot* slots = nullptr;
@@ -758,7 +760,9 @@ bool use_sorted_k3(const rg_ctx* ctx) {
     return ctx->p.distance <= 2 && ctx->used < 0x7fffffffull;  // S <= D = used
 }
 
-rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
+// K2 (+ window_fix / dedupe pre-passes) enqueued on the stream; the
+// significant count stays on the device (ctr->n_sig).
+rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
     if (ctx->state != rg_ctx::kAccum) {
         // prune() on a consumed accumulator returns nothing (empty table).
         rg_status s = reopen_accumulator(ctx);
@@ -766,7 +770,6 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
     }
     rg_status s = ensure_sig_capacity(ctx, ctx->used);
     if (s != RG_OK) return s;
-    PhaseTimer timer(ctx, &ctx->ms_prune);
     zero_field(ctx, &ctx->ctr->n_sig);
     if (ctx->slots && ctx->used) {
         const bool hash_k3 = !use_sorted_k3(ctx);
@@ -793,6 +796,13 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
                           ctx->root_cid, ctx->ctr, ctx->n_sm, ctx->st));
         ++ctx->launches;
     }
+    return RG_OK;
+}
+
+rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
+    PhaseTimer timer(ctx, &ctx->ms_prune);
+    rg_status s = prune_enqueue(ctx, window_fix);
+    if (s != RG_OK) return s;
     CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, sizeof(u64), cudaMemcpyDeviceToHost,
                        ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -808,8 +818,12 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
 }
 
 
-rg_status agglomerate_sorted_impl(rg_ctx* ctx) {
-    const u64 n = ctx->n_sig;
+// Sorted K3. n = an upper bound of the significant count when `fused` (the
+// kernels read the exact count from ctr->n_sig; CUB calls cover the bound,
+// and entries past the count are never read back); results are read back by
+// the caller then.
+rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused = false) {
+    const u64 n = fused ? n_bound : ctx->n_sig;
     const int kb = (int)(ctx->res.bits_x + ctx->res.bits_y);
     if (ctx->s_cap < n || !ctx->s_flag) {
         dfree(ctx->s_flag);
@@ -881,6 +895,7 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx) {
     zero_field(ctx, &ctx->ctr->n_kept);
     CK(launch_agglomerate_sorted(L, ctx->st));
     ctx->launches += 14;  // iota + radix sort (6) + union, edges, reduce, flags, scan (2), label
+    if (fused) return RG_OK;
     CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
                        cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -1102,6 +1117,9 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
     if ((e = cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(e, "stream");
     if ((e = cudaEventCreate(&ctx->t0)) != cudaSuccess) return fail(e, "event");
+    if ((e = cudaEventCreate(&ctx->ev_k2)) != cudaSuccess) return fail(e, "event");
+    if ((e = cudaEventCreate(&ctx->ev_k3)) != cudaSuccess) return fail(e, "event");
+    if ((e = cudaEventCreate(&ctx->ev_end)) != cudaSuccess) return fail(e, "event");
     if ((e = cudaEventCreate(&ctx->t1)) != cudaSuccess) return fail(e, "event");
     for (int b = 0; b < 2; ++b) {
         if ((e = cudaEventCreateWithFlags(&ctx->copied[b], cudaEventDisableTiming)) !=
@@ -1176,6 +1194,9 @@ void rg_destroy(rg_ctx* ctx) {
         if (ctx->done[b]) cudaEventDestroy(ctx->done[b]);
     }
     if (ctx->t0) cudaEventDestroy(ctx->t0);
+    if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
+    if (ctx->ev_k3) cudaEventDestroy(ctx->ev_k3);
+    if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
     if (ctx->t1) cudaEventDestroy(ctx->t1);
     if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -1616,6 +1637,46 @@ rg_status rg_get_stats(rg_ctx* ctx, rg_stats* out) {
     return RG_OK;
 }
 
+// cluster_sequential's prune + agglomerate on the sorted K3 path with one
+// host synchronisation at the end: K2 leaves the significant count on the
+// device and K3 is sized by the entry count (its upper bound). Phase times
+// come from events read after the final synchronisation.
+rg_status prune_agglomerate_fused(rg_ctx* ctx, bool window_fix) {
+    CK(cudaEventRecord(ctx->ev_k2, ctx->st));
+    rg_status s = prune_enqueue(ctx, window_fix);
+    if (s != RG_OK) return s;
+    CK(cudaEventRecord(ctx->ev_k3, ctx->st));
+    const u64 bound = ctx->used;
+    ctx->n_roots = ctx->n_kept = 0;
+    if (bound) {
+        s = agglomerate_sorted_impl(ctx, bound, true);
+        if (s != RG_OK) return s;
+    } else {
+        zero_field(ctx, &ctx->ctr->n_roots);
+        zero_field(ctx, &ctx->ctr->n_kept);
+    }
+    CK(cudaEventRecord(ctx->ev_end, ctx->st));
+    static_assert(offsetof(Counters, n_kept) == offsetof(Counters, n_sig) + 2 * sizeof(u64),
+                  "n_sig, n_roots, n_kept are adjacent");
+    CK(cudaMemcpyAsync(&ctx->hctr->n_sig, &ctx->ctr->n_sig, 3 * sizeof(u64),
+                       cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ctx->ev_k2, ctx->ev_k3);
+    cudaEventElapsedTime(&b, ctx->ev_k3, ctx->ev_end);
+    ctx->ms_prune += a;
+    ctx->ms_agg += b;
+    ctx->n_sig = ctx->hctr->n_sig;
+    ctx->n_roots = ctx->hctr->n_roots;
+    ctx->n_kept = ctx->hctr->n_kept;
+    ctx->table_dirty = true;
+    ctx->res = ctx->grid;
+    ctx->res_is_canvas = true;
+    ctx->sorted = bound != 0;
+    ctx->state = rg_ctx::kAgg;
+    return RG_OK;
+}
+
 static rg_status reset_impl(rg_ctx* ctx) {
     ctx->state = rg_ctx::kAccum;
     ctx->table_dirty = true;
@@ -1650,10 +1711,16 @@ rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind ki
     s = ingest_any(ctx, xy, n, kind);
     if (s != RG_OK) return s;
     const u64 peak = ctx->used;
-    s = prune_impl(ctx, (flags & RG_CLUSTER_WINDOW_FIX) != 0);
-    if (s != RG_OK) return s;
-    s = agglomerate_impl(ctx);
-    if (s != RG_OK) return s;
+    const bool wf = (flags & RG_CLUSTER_WINDOW_FIX) != 0;
+    if (use_sorted_k3(ctx)) {
+        s = prune_agglomerate_fused(ctx, wf);
+        if (s != RG_OK) return s;
+    } else {
+        s = prune_impl(ctx, wf);
+        if (s != RG_OK) return s;
+        s = agglomerate_impl(ctx);
+        if (s != RG_OK) return s;
+    }
     ctx->used = peak;  // peak_accumulator_entries pipeline.hpp:100
     if (stats) return rg_get_stats(ctx, stats);
     return RG_OK;
