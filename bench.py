@@ -284,10 +284,9 @@ def ours(args) -> None:
     # canonical result (sorted significant tiles + counts + cluster ids) back.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     S = st.n_significant
-    tx = np.empty(S, np.int64)
-    ty = np.empty(S, np.int64)
-    cnt = np.empty(S, np.uint64)
-    cid = np.empty(S, np.int64)
+    # the result lands in pinned host buffers (as the input comes from one)
+    pinned = [torch.empty(max(S, 1), dtype=torch.int64, pin_memory=True) for _ in range(4)]
+    tx, ty, cnt, cid = (p.numpy() for p in pinned)
     from paper_1907_03620_b200 import _native as N
 
     barrier()

@@ -243,6 +243,20 @@ cudaError_t dalloc(T** p, u64 count) {
     return cudaMalloc((void**)p, count * sizeof(T));
 }
 
+// Stream-ordered temporaries (pooled by the device's default memory pool,
+// whose release threshold rg_create raises, so per-call scratch does not pay
+// cudaMalloc/cudaFree).
+template <typename T>
+cudaError_t salloc(T** p, u64 count, cudaStream_t st) {
+    *p = nullptr;
+    return cudaMallocAsync((void**)p, (size_t)std::max<u64>(count, 1) * sizeof(T), st);
+}
+template <typename T>
+void sfree(T*& p, cudaStream_t st) {
+    if (p) cudaFreeAsync((void*)p, st);
+    p = nullptr;
+}
+
 template <typename T>
 void dfree(T*& p) {
     if (p) cudaFree((void*)p);
@@ -1091,6 +1105,15 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
                        "device %d is sm_%d%d; this library is built for sm_100a only", device,
                        prop.major, prop.minor);
     DevGuard guard(device);
+    {
+        // keep freed stream-ordered scratch in the pool (see salloc)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            u64 keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     rg_ctx* ctx = new rg_ctx();
     ctx->p = *p;
     ctx->device = device;
@@ -1756,10 +1779,10 @@ rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* co
     if (kind == RG_MEM_HOST) {
         dtx = dty = dcid = nullptr;
         dcnt = nullptr;
-        if (tx) CK(dalloc(&dtx, w));
-        if (ty) CK(dalloc(&dty, w));
-        if (count) CK(dalloc(&dcnt, w));
-        if (cluster_id) CK(dalloc(&dcid, w));
+        if (tx) CK(salloc(&dtx, w, ctx->st));
+        if (ty) CK(salloc(&dty, w, ctx->st));
+        if (count) CK(salloc(&dcnt, w, ctx->st));
+        if (cluster_id) CK(salloc(&dcid, w, ctx->st));
     }
     CK(launch_gather_sorted(order, ctx->sig_key, ctx->sig_cnt,
                             ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr, w, ctx->res,
@@ -1771,13 +1794,13 @@ rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* co
         if (count) CK(cudaMemcpyAsync(count, dcnt, w * 8, cudaMemcpyDeviceToHost, ctx->st));
         if (cluster_id) CK(cudaMemcpyAsync(cluster_id, dcid, w * 8, cudaMemcpyDeviceToHost, ctx->st));
     }
-    CK(cudaStreamSynchronize(ctx->st));
     if (kind == RG_MEM_HOST) {
-        dfree(dtx);
-        dfree(dty);
-        dfree(dcnt);
-        dfree(dcid);
+        sfree(dtx, ctx->st);
+        sfree(dty, ctx->st);
+        sfree(dcnt, ctx->st);
+        sfree(dcid, ctx->st);
     }
+    CK(cudaStreamSynchronize(ctx->st));
     if (temp) cudaFree(temp);
     dfree(ks);
     dfree(iota);

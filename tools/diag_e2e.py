@@ -26,3 +26,6 @@ S = st.n_significant
 tx = np.empty(S, np.int64); ty = np.empty(S, np.int64); cnt = np.empty(S, np.uint64); cid = np.empty(S, np.int64)
 print('get_significant ms', t(lambda: pl.ctx.lib.rg_get_significant(pl.ctx.h, tx.ctypes.data, ty.ctypes.data, cnt.ctypes.data, cid.ctypes.data, S, N.RG_MEM_HOST)))
 print('torch h2d 8GB ms', t(lambda: dev.copy_(host, non_blocking=True)))
+ptx = torch.empty(S, dtype=torch.int64, pin_memory=True); pty = torch.empty(S, dtype=torch.int64, pin_memory=True)
+pcnt = torch.empty(S, dtype=torch.int64, pin_memory=True); pcid = torch.empty(S, dtype=torch.int64, pin_memory=True)
+print('get_significant pinned ms', t(lambda: pl.ctx.lib.rg_get_significant(pl.ctx.h, ptx.data_ptr(), pty.data_ptr(), pcnt.data_ptr(), pcid.data_ptr(), S, N.RG_MEM_HOST)))
