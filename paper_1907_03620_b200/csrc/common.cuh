@@ -218,6 +218,75 @@ __device__ __forceinline__ u64 table_claim(const Table& t, u64 key) {
     }
 }
 
+// Cache keys. In the narrow case (every canvas column/row index fits int32,
+// checked on the host) the per-warp cache works on the unpacked pair
+// (kx << 32 | ky): building it costs no shift, its slot is two bit
+// operations, and the table's packed key (kx << bits_y | ky) is formed only
+// when an entry leaves the cache. Otherwise the packed key is used
+// throughout. Out-of-bounds points get kEmpty (a valid pair has kx < 2^31).
+template <bool kNarrow>
+struct KeyOps;
+
+template <>
+struct KeyOps<true> {
+    __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
+        const int tx = __double2int_rd(__dmul_rn(x, g.scale));
+        const int ty = __double2int_rd(__dmul_rn(y, g.scale));
+        const u32 kx = (u32)(tx - (int)g.origin_x);
+        const u32 ky = (u32)(ty - (int)g.origin_y);
+        return in_bounds(g, x, y) ? (((u64)kx << 32) | ky) : kEmpty;
+    }
+    // Direct-mapped by position in an 8 x 16-tile window (low 3 column bits,
+    // low 4 row bits): the few tiles of one cluster never evict each other.
+    __device__ static __forceinline__ u32 slot(u64 ck, u32) {
+        return (((u32)(ck >> 32) & 7u) << 4) | ((u32)ck & 15u);
+    }
+    __device__ static __forceinline__ u64 table_key(u64 ck, u32 bits_y) {
+        return ck == kEmpty ? kEmpty : (((ck >> 32) << bits_y) | (u32)ck);
+    }
+};
+
+template <>
+struct KeyOps<false> {
+    __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
+        const u64 k = pack_key(g, x, y);
+        return in_bounds(g, x, y) ? k : kEmpty;
+    }
+    __device__ static __forceinline__ u32 slot(u64 k, u32 bits_y) {
+        return (((u32)(k >> bits_y) & 7u) << 4) | ((u32)k & 15u);
+    }
+    __device__ static __forceinline__ u64 table_key(u64 k, u32) { return k; }
+};
+
+__device__ __forceinline__ u32 match_any64(u64 v) {
+    u32 m;
+    asm volatile("match.any.sync.b64 %0, %1, 0xffffffff;" : "=r"(m) : "l"(v));
+    return m;
+}
+
+__device__ __forceinline__ u32 ballot(bool p) {
+    u32 m;
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n vote.sync.ballot.b32 %0, q, 0xffffffff;\n}"
+        : "=r"(m)
+        : "r"((u32)p));
+    return m;
+}
+
+// Asynchronous 16-byte global->shared copy (LDGSTS), L1-bypassing, with an
+// L2 evict-first policy: the points are read exactly once.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, u64 pol) {
+    const u32 s = (u32)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Device-side counters of one context (one cache line each to avoid false
 // sharing between the hot ones).
 struct Counters {

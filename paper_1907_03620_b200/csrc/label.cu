@@ -20,114 +20,59 @@
 
 namespace rg {
 
-constexpr int kLWarps = 8;
+constexpr int kLWarps = 4;
 constexpr int kLBatch = 2;
+constexpr int kLRing = 4;     // rows in flight per warp (cp.async ring)
 constexpr int kLCache = 128;
-constexpr u64 kLRowsPerSeg = 64;
-
-struct LRows {
-    double x[kLBatch], y[kLBatch];
-};
-
-template <bool kAligned>
-__device__ __forceinline__ void l_load(const double* xy, u64 p0, u32 left, int lane, u64 pol,
-                                       LRows& o) {
-    if (kAligned && left == 32 * kLBatch) {
-        const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
-#pragma unroll
-        for (int b = 0; b < kLBatch; ++b) {
-            const double2 v = ld_point_stream(base + b * 32, pol);
-            o.x[b] = v.x;
-            o.y[b] = v.y;
-        }
-        return;
-    }
-#pragma unroll
-    for (int b = 0; b < kLBatch; ++b) {
-        if ((u32)(b * 32 + lane) < left) {
-            if (kAligned) {
-                const double2 v =
-                    ld_point_stream(reinterpret_cast<const double2*>(xy) + p0 + b * 32 + lane, pol);
-                o.x[b] = v.x;
-                o.y[b] = v.y;
-            } else {
-                const double* q = xy + 2 * (p0 + b * 32 + lane);
-                o.x[b] = q[0];
-                o.y[b] = q[1];
-            }
-        } else {
-            o.x[b] = o.y[b] = __longlong_as_double(0x7ff8000000000000ll);
-        }
-    }
-}
+constexpr u32 kLRowsPerSeg = 256;
 
 struct LSmem {
-    u64 ckey[kLCache];
+    u64 ckey[kLCache];  // cache keys (KeyOps) -> cluster id
     int ccid[kLCache];
     unsigned char owner[kLCache];
 };
 
-__device__ __forceinline__ u32 l_slot(u64 key, u32 bits_y) {
-    return (((u32)(key >> bits_y) & 7u) << 4) | ((u32)key & 15u);
-}
-
+// One row: every lane looks its tile up in the per-warp cache (direct-mapped
+// by position in an 8 x 16-tile window, as in K1); lanes that miss probe the
+// table themselves (equal keys in a row probe the same lines) and one lane
+// per slot installs the result.
 template <bool kNarrow>
-__device__ __forceinline__ u64 l_key(const Grid& g, double x, double y) {
-    if (kNarrow) {
-        const int tx = __double2int_rd(__dmul_rn(x, g.scale));
-        const int ty = __double2int_rd(__dmul_rn(y, g.scale));
-        return ((u64)(u32)(tx - (int)g.origin_x) << g.bits_y) | (u32)(ty - (int)g.origin_y);
-    }
-    return pack_key(g, x, y);
-}
-
-template <bool kNarrow>
-__device__ __forceinline__ void l_batch(const Grid& g, const Table& t, const int* tile_cid,
-                                        const LRows& cur, u64 p0, u32 left, LSmem& w, int lane,
-                                        u32 lane_bit, int* labels) {
-#pragma unroll
-    for (int b = 0; b < kLBatch; ++b) {
-        const bool inb = in_bounds(g, cur.x[b], cur.y[b]);
-        const u64 kk = l_key<kNarrow>(g, cur.x[b], cur.y[b]);
-        const u64 key = inb ? kk : kEmpty;
-        const u32 peers = __match_any_sync(kFull, key);
-        const int leader_lane = __ffs(peers) - 1;
-        const bool leader = inb && ((peers & (0u - peers)) == lane_bit);
-        const u32 cs = l_slot(key, g.bits_y);
-        int cid = -1;
-        bool miss = false;
-        if (leader) {
-            if (w.ckey[cs] == key)
-                cid = w.ccid[cs];
-            else
-                miss = true;
-        }
-        if (__any_sync(kFull, miss)) {
-            if (miss) {
-                const u64 v = table_find(t, key);
-                cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
-                w.owner[cs] = (unsigned char)lane;
-            }
-            __syncwarp();
-            if (miss && w.owner[cs] == lane) {
-                w.ckey[cs] = key;
-                w.ccid[cs] = cid;
-            }
+__device__ __forceinline__ int l_row(const Grid& g, const Table& t, const int* tile_cid, double x,
+                                     double y, LSmem& w, int lane) {
+    using K = KeyOps<kNarrow>;
+    const u64 key = K::cache_key(g, x, y);
+    const bool valid = key != kEmpty;
+    const u32 cs = K::slot(key, g.bits_y);
+    const bool hit = valid && w.ckey[cs] == key;
+    int cid = hit ? w.ccid[cs] : -1;
+    const bool miss = valid && !hit;
+    if (ballot(miss)) {
+        if (miss) {
+            const u64 v = table_find(t, K::table_key(key, g.bits_y));
+            cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
+            w.owner[cs] = (unsigned char)lane;
         }
         __syncwarp();
-        cid = __shfl_sync(kFull, cid, leader_lane);
-        if ((u32)(b * 32 + lane) < left) labels[p0 + b * 32 + lane] = inb ? cid : -1;
+        if (miss && w.owner[cs] == lane) {
+            w.ckey[cs] = key;
+            w.ccid[cs] = cid;
+        }
+        __syncwarp();
     }
+    return cid;
 }
 
+// Segments of kLRowsPerSeg rows are dealt to warps round-robin; each warp
+// streams its rows through a per-lane cp.async ring like K1.
 template <bool kAligned, bool kNarrow>
-__global__ void __launch_bounds__(kLWarps * 32) k_label_points(const double* xy, u64 n, Grid g,
-                                                               Table t, const int* tile_cid,
-                                                               int* labels) {
+__global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* xy, u64 n, Grid g,
+                                                                  Table t, const int* tile_cid,
+                                                                  int* labels) {
     __shared__ LSmem s_warp[kLWarps];
+    __shared__ __align__(16) double2 s_ring[kLWarps][kLRing][32];
     const int lane = threadIdx.x & 31;
-    const u32 lane_bit = 1u << lane;
     LSmem& w = s_warp[threadIdx.x >> 5];
+    double2 (*ring)[32] = s_ring[threadIdx.x >> 5];
     for (int i = lane; i < kLCache; i += 32) w.ckey[i] = kEmpty;
     __syncwarp();
     const u64 pol = evict_first_policy();
@@ -136,27 +81,52 @@ __global__ void __launch_bounds__(kLWarps * 32) k_label_points(const double* xy,
     const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
     const u64 n_warps = ((u64)gridDim.x * blockDim.x) >> 5;
     for (u64 seg = warp; seg < n_seg; seg += n_warps) {
-        const u64 p_end = min((seg + 1) * kLRowsPerSeg * 32, n);
-        u64 p0 = seg * kLRowsPerSeg * 32;
-        u32 left = (u32)min(p_end - p0, (u64)(32 * kLBatch));
-        LRows ra, rb;
-        l_load<kAligned>(xy, p0, left, lane, pol, ra);
-        while (true) {
-            u64 pn = p0 + 32 * kLBatch;
-            u32 left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kLBatch)) : 0u;
-            if (left_n) l_load<kAligned>(xy, pn, left_n, lane, pol, rb);
-            l_batch<kNarrow>(g, t, tile_cid, ra, p0, left, w, lane, lane_bit, labels);
-            if (!left_n) break;
-            p0 = pn;
-            left = left_n;
-            pn = p0 + 32 * kLBatch;
-            left_n = pn < p_end ? (u32)min(p_end - pn, (u64)(32 * kLBatch)) : 0u;
-            if (left_n) l_load<kAligned>(xy, pn, left_n, lane, pol, ra);
-            l_batch<kNarrow>(g, t, tile_cid, rb, p0, left, w, lane, lane_bit, labels);
-            if (!left_n) break;
-            p0 = pn;
-            left = left_n;
+        const u64 p0 = seg * kLRowsPerSeg * 32;
+        const u32 valid = (u32)min(n - p0, (u64)kLRowsPerSeg * 32);
+        const u32 nr = (valid + 31) / 32;
+        const double2* base = reinterpret_cast<const double2*>(xy) + p0 + lane;
+        const double* xb = xy + 2 * p0;
+        int* lab = labels + p0 + lane;
+        auto issue = [&](u32 row) {
+            if (row < nr) {
+                const u32 idx = row * 32 + lane;
+                if (idx < valid) {
+                    double2* dst = &ring[row % kLRing][lane];
+                    if (kAligned) {
+                        cp_async16(dst, base + row * 32, pol);
+                    } else {
+                        dst->x = xb[2 * (u64)idx];
+                        dst->y = xb[2 * (u64)idx + 1];
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int k = 0; k < kLRing; ++k) issue(k);
+        for (u32 j = 0; j < nr; j += kLBatch) {
+            cp_async_wait<kLRing - kLBatch>();
+            double x[kLBatch], y[kLBatch];
+#pragma unroll
+            for (int b = 0; b < kLBatch; ++b) {
+                const u32 row = j + b;
+                if (row * 32 + lane < valid) {
+                    const double2 v = ring[row % kLRing][lane];
+                    x[b] = v.x;
+                    y[b] = v.y;
+                } else {
+                    x[b] = y[b] = __longlong_as_double(0x7ff8000000000000ll);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < kLBatch; ++b) issue(j + kLRing + b);
+#pragma unroll
+            for (int b = 0; b < kLBatch; ++b) {
+                const int cid = l_row<kNarrow>(g, t, tile_cid, x[b], y[b], w, lane);
+                if ((j + b) * 32 + lane < valid) lab[(j + b) * 32] = cid;
+            }
         }
+        cp_async_wait<0>();
     }
 }
 
