@@ -289,6 +289,7 @@ def ours(args) -> None:
     tx, ty, cnt, cid = (p.numpy() for p in pinned)
     from paper_1907_03620_b200 import _native as N
 
+    pl.run(host)  # untimed: first host-path call allocates the staging buffers
     barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
