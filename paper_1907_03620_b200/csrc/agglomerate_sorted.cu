@@ -453,24 +453,45 @@ __global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt,
     if (lane == 0 && mx) atomicMax(max_col, mx);
 }
 
-__global__ void k_col_scatter(const u64* key, const u64* n_p, u32 bits_y, u32* cursor,
-                              u64* k_out, u32* v_out) {
+// Each thread scatters kColIlp keys of a warp tile whose reservations are in
+// flight together (the reservation's round trip, not bandwidth, bounds a
+// one-key-per-iteration scatter).
+constexpr int kColIlp = 4;
+__global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* n_p, u32 bits_y,
+                                                     u32* cursor, u64* k_out, u32* v_out) {
     const u64 n = *n_p;
     const int lane = threadIdx.x & 31;
-    const u64 span = (n + 31) / 32 * 32;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
-         i += (u64)gridDim.x * blockDim.x) {
-        const bool valid = i < n;
-        const u64 k = valid ? key[i] : 0;
-        const u32 col = valid ? (u32)(k >> bits_y) : 0xffffffffu;
-        const u32 peers = __match_any_sync(kFull, col);
-        const int leader = __ffs(peers) - 1;
-        u32 at = 0;
-        if (valid && lane == leader) at = atomicAdd(cursor + col, (u32)__popc(peers));
-        at = __shfl_sync(kFull, at, leader) + __popc(peers & ((1u << lane) - 1));
-        if (valid) {
-            k_out[at] = k;
-            v_out[at] = (u32)i;
+    const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+    const u64 n_warps = ((u64)gridDim.x * blockDim.x) >> 5;
+    constexpr u64 tile = 32ull * kColIlp;
+    for (u64 base = warp * tile; base < n; base += n_warps * tile) {
+        u64 k[kColIlp];
+        u32 col[kColIlp], peers[kColIlp], at[kColIlp];
+#pragma unroll
+        for (int j = 0; j < kColIlp; ++j) {
+            const u64 i = base + j * 32 + lane;
+            k[j] = i < n ? key[i] : 0;
+            col[j] = i < n ? (u32)(k[j] >> bits_y) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < kColIlp; ++j) peers[j] = __match_any_sync(kFull, col[j]);
+#pragma unroll
+        for (int j = 0; j < kColIlp; ++j) {
+            const int leader = __ffs(peers[j]) - 1;
+            at[j] = 0;
+            if (col[j] != 0xffffffffu && lane == leader)
+                at[j] = atomicAdd(cursor + col[j], (u32)__popc(peers[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < kColIlp; ++j) {
+            const int leader = __ffs(peers[j]) - 1;
+            const u32 pos = __shfl_sync(kFull, at[j], leader) +
+                            __popc(peers[j] & ((1u << lane) - 1));
+            const u64 i = base + j * 32 + lane;
+            if (i < n) {
+                k_out[pos] = k[j];
+                v_out[pos] = (u32)i;
+            }
         }
     }
 }
