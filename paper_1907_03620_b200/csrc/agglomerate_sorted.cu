@@ -16,6 +16,10 @@
 //     flags — no per-root minimum and no sort of the roots;
 //   * the sorted keys are the canonical output order.
 // Used for delta <= 2 (at most 12 forward offsets, bounded edge list).
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -496,89 +500,6 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
     }
 }
 
-// Sort each column by row (columns of <= 256 tiles): one warp per column,
-// bitonic network in registers (<= 32) or in the warp's shared buffer.
-constexpr int kColSortMax = 256;
-// Measured on config 4 (8.75M tiles, ~360K columns): CUB's segmented sort
-// 211 us, this warp-per-column kernel 287 us (latency-bound on tiny
-// columns), so it is off by default.
-constexpr bool kUseWarpColumnSort = false;
-__global__ void __launch_bounds__(256) k_col_sort(const u32* off, u64 cols, const u64* k_in,
-                                                  const u32* v_in, u64* k_out, u32* v_out) {
-    __shared__ u64 s_k[8][kColSortMax];
-    __shared__ u32 s_v[8][kColSortMax];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u64* sk = s_k[wid];
-    u32* sv = s_v[wid];
-    for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c < cols;
-         c += ((u64)gridDim.x * blockDim.x) >> 5) {
-        const u32 b = off[c], e = off[c + 1];
-        const u32 n = e - b;
-        if (n == 0) continue;
-        if (n == 1) {
-            if (lane == 0) {
-                k_out[b] = k_in[b];
-                v_out[b] = v_in[b];
-            }
-            continue;
-        }
-        if (n <= 32) {
-            u64 k = lane < (int)n ? k_in[b + lane] : ~0ull;
-            u32 v = lane < (int)n ? v_in[b + lane] : 0;
-#pragma unroll
-            for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    const u64 ok = __shfl_xor_sync(kFull, k, stride);
-                    const u32 ov = __shfl_xor_sync(kFull, v, stride);
-                    const bool up = ((lane & size) == 0);
-                    const bool lower = (lane & stride) == 0;
-                    const bool take = lower ? (up ? ok < k : ok > k) : (up ? ok > k : ok < k);
-                    if (take) {
-                        k = ok;
-                        v = ov;
-                    }
-                }
-            }
-            if (lane < (int)n) {
-                k_out[b + lane] = k;
-                v_out[b + lane] = v;
-            }
-            continue;
-        }
-        u32 N = 64;
-        while (N < n) N <<= 1;
-        for (u32 q = lane; q < N; q += 32) {
-            sk[q] = q < n ? k_in[b + q] : ~0ull;
-            sv[q] = q < n ? v_in[b + q] : 0;
-        }
-        __syncwarp();
-        for (u32 size = 2; size <= N; size <<= 1)
-            for (u32 stride = size >> 1; stride > 0; stride >>= 1) {
-                for (u32 q = lane; q < N; q += 32) {
-                    const u32 p = q ^ stride;
-                    if (p > q) {
-                        const bool up = (q & size) == 0;
-                        const u64 a = sk[q], bb = sk[p];
-                        if (up ? a > bb : a < bb) {
-                            sk[q] = bb;
-                            sk[p] = a;
-                            const u32 t = sv[q];
-                            sv[q] = sv[p];
-                            sv[p] = t;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        for (u32 q = lane; q < n; q += 32) {
-            k_out[b + q] = sk[q];
-            v_out[b + q] = sv[q];
-        }
-        __syncwarp();
-    }
-}
-
 static int grid_for_s(u64 n, int n_sm, int per_sm) {
     const u64 want = (n + 255) / 256;
     const u64 cap = (u64)n_sm * per_sm;
@@ -604,42 +525,49 @@ size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x) {
     return std::max(std::max(a, b), std::max(c, d));
 }
 
+// Columns longer than this reach CUB's large-segment path, which sorts all 64
+// key bits per segment and is slow
+// (config 5's walks: 2.7 ms); such inputs take the full radix sort instead.
+#ifndef RG_SEG_MAX_COLUMN
+#define RG_SEG_MAX_COLUMN 128
+#endif
+constexpr u64 kSegSortMaxColumn = RG_SEG_MAX_COLUMN;
+
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
-    const u64 n = L.n_sig;
-    if (n == 0) return cudaSuccess;
-    const int gs = grid_for_s(n, L.n_sm, 16);
+    if (L.n_sig == 0) return cudaSuccess;
     cudaError_t e;
     size_t bytes = L.temp_bytes;
     const u64 cols = sorted_columns(L.key_bits - L.bits_y);
     if (cols && L.col_cnt) {
         cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
         cudaMemsetAsync(&L.ctr->max_col, 0, sizeof(u64), st);
-        k_col_hist<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt,
-                                       (u32*)&L.ctr->max_col);
+        k_col_hist<<<grid_for_s(L.n_sig, L.n_sm, 16), 256, 0, st>>>(
+            L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, (u32*)&L.ctr->max_col);
+    }
+    // The exact significant count (L.n_sig may be an upper bound) and the
+    // longest column decide the sort and size every launch below.
+    if ((e = cudaMemcpyAsync(&L.host_ctr->n_sig, &L.ctr->n_sig,
+                             sizeof(Counters) - offsetof(Counters, n_sig),
+                             cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    const u64 n = L.host_ctr->n_sig;
+    if (std::getenv("RG_DEBUG"))
+        std::fprintf(stderr, "[rg] K3 sorted: n=%llu max_col=%llu\n", (unsigned long long)n,
+                     (unsigned long long)L.host_ctr->max_col);
+    if (n == 0) return cudaSuccess;
+    const int gs = grid_for_s(n, L.n_sm, 16);
+    if (cols && L.col_cnt && L.host_ctr->max_col <= kSegSortMaxColumn) {
         e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
         if (e != cudaSuccess) return e;
         cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
                         st);
         k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
                                           L.iota);
-        u64 max_col = ~0ull;
-        if (kUseWarpColumnSort) {
-            cudaMemcpyAsync(&max_col, &L.ctr->max_col, sizeof(u64), cudaMemcpyDeviceToHost, st);
-            e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return e;
-        }
-        if (kUseWarpColumnSort && max_col <= (u64)kColSortMax) {
-            const u64 want = (cols * 32 + 255) / 256;
-            const u64 capb = (u64)L.n_sm * 8;
-            k_col_sort<<<(int)(want < capb ? (want ? want : 1) : capb), 256, 0, st>>>(
-                L.col_off, cols, L.ktmp, L.iota, L.skey, L.perm);
-        } else {
-            bytes = L.temp_bytes;
-            e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
-                                                    (int)n, (int)cols, L.col_off, L.col_off + 1,
-                                                    st);
-            if (e != cudaSuccess) return e;
-        }
+        bytes = L.temp_bytes;
+        e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
+                                                (int)n, (int)cols, L.col_off, L.col_off + 1, st);
+        if (e != cudaSuccess) return e;
     } else {
         e = launch_iota(L.iota, n, L.n_sm, st);
         if (e != cudaSuccess) return e;

@@ -904,6 +904,7 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     L.temp = ctx->sort_temp;
     L.temp_bytes = ctx->sort_temp_bytes;
     L.ctr = ctx->ctr;
+    L.host_ctr = ctx->hctr;
     L.n_sm = ctx->n_sm;
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);

@@ -100,6 +100,7 @@ struct SortedLaunch {
     void* temp;
     size_t temp_bytes;
     Counters* ctr;
+    Counters* host_ctr;   // pinned mirror: the exact count is read back once
     int n_sm;
 };
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
