@@ -178,7 +178,33 @@ int main() {
             CHECK(s_ref.n_significant == s_gpu.n_significant, "window_fix n_significant");
         }
     }
-    // 7. Config errors are ConfigError.
+    // 7. Single pass over a PointSource (CountingSource io.hpp:63-84, as
+    //    test_pipeline.cpp:68-82) through both the span fast path and the
+    //    chunked path (a stream-only source, test_parallel.cpp:40-47), with
+    //    prime mode on the chunked path.
+    {
+        struct StreamOnly : PointSource {
+            explicit StreamOnly(std::span<const Point> p) : src(p) {}
+            std::size_t read(std::span<Point> out) override { return src.read(out); }
+            VectorSource src;
+        };
+        const auto pts = gaussian_clusters(300, 4000, 0.0005, 4242, 0.05);  // > 1 Mi points
+        for (int prime = 0; prime < 2; ++prime) {
+            GridParams params;
+            params.precision = 3.0;
+            if (prime) params.mode = Mode::retain_points;
+            const ClusterSet want = raster::cluster_sequential(pts, params);
+            VectorSource vs(pts);
+            CountingSource cs1(vs);
+            CHECK(raster::gpu::cluster_sequential(cs1, params) == want, "span source");
+            CHECK(cs1.points_read() == pts.size(), "span source read once");
+            StreamOnly so(pts);
+            CountingSource cs2(so);
+            CHECK(raster::gpu::cluster_sequential(cs2, params) == want, "stream-only source");
+            CHECK(cs2.points_read() == pts.size(), "stream-only source read once");
+        }
+    }
+    // 8. Config errors are ConfigError.
     {
         GridParams bad;
         bad.threshold = 0;

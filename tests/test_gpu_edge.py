@@ -245,3 +245,43 @@ def test_lattice_same_block_position():
     flat = cluster_flat(pts, gp)
     assert_same(flat, oracle(pts, gp))
     assert flat.n_clusters == 160_000
+
+
+@pytest.mark.parametrize("metric,delta", [(Metric.chebyshev, 1), (Metric.manhattan, 1),
+                                          (Metric.chebyshev, 2), (Metric.manhattan, 2),
+                                          (Metric.chebyshev, 3)])
+def test_adjacency_per_offset(metric, delta):
+    """neighbor_offsets agglomerate.hpp:38-50 as the device sees it: two tiles
+    form one cluster exactly when their offset is in the neighbourhood
+    (test_agglomerate.cpp:30-62)."""
+    gp = GridParams(metric=metric, distance=delta, min_cluster_size=1)
+    for dx in range(-4, 5):
+        for dy in range(-4, 5):
+            if dx == 0 and dy == 0:
+                continue
+            flat = agglomerate_flat({Tile(100, 100): 5, Tile(100 + dx, 100 + dy): 5}, gp)
+            near = (max(abs(dx), abs(dy)) if metric == Metric.chebyshev else abs(dx) + abs(dy)) <= delta
+            assert flat.n_clusters == (1 if near else 2), (metric, delta, dx, dy)
+
+
+def test_threshold_one_keeps_every_occupied_tile():
+    """test_accumulator.cpp:135-143"""
+    rng = np.random.default_rng(11)
+    gp = GridParams(precision=2, threshold=1)
+    acc = TileAccumulator(gp)
+    acc.ingest(rng.uniform(-10, 10, size=(300, 2)))
+    occupied = acc.entry_count()
+    assert len(acc.prune()) == occupied
+
+
+def test_dense_cluster_yields_a_significant_tile():
+    """test_accumulator.cpp:145-165 (500 points in a square of half-side
+    ~2.5 tile sides at p=3.5, tau=5)."""
+    rng = np.random.default_rng(2024)
+    r = 2.5e-3 / 3.1622776601683795
+    pts = 1.0 + rng.uniform(-r, r, size=(500, 2))
+    gp = GridParams(precision=3.5, threshold=5)
+    assert max(numpy_tile_counts(pts, gp).values()) >= 5
+    acc = TileAccumulator(gp)
+    acc.ingest(pts)
+    assert len(acc.prune()) >= 1

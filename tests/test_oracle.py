@@ -228,3 +228,17 @@ def test_dedupe_vs_live_reference():
         assert np.array_equal(mine.cluster_id, ref.cluster_id), trial
         plain = O.port_cluster(pts, gp, window_fix=wf)
         assert mine.tx.size <= plain.tx.size
+
+
+def test_neighbor_offsets_kats():
+    """test_agglomerate.cpp:30-62 on the Python mirror's neighbor_offsets."""
+    from paper_1907_03620_b200.raster import Tile, neighbor_offsets
+
+    cheb1 = {(t.x, t.y) for t in neighbor_offsets(GridParams())}
+    assert cheb1 == {(-1, -1), (-1, 0), (-1, 1), (0, -1), (0, 1), (1, -1), (1, 0), (1, 1)}
+    man1 = {(t.x, t.y) for t in neighbor_offsets(GridParams(metric=Metric.manhattan))}
+    assert man1 == {(-1, 0), (1, 0), (0, -1), (0, 1)}
+    assert len(neighbor_offsets(GridParams(distance=2))) == 24
+    man2 = neighbor_offsets(GridParams(metric=Metric.manhattan, distance=2))
+    assert len(man2) == 12 and all(abs(t.x) + abs(t.y) <= 2 for t in man2)
+    assert Tile(0, 0) not in set(man2)
