@@ -23,6 +23,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -395,36 +397,42 @@ __global__ void k_sorted_reduce(u32* parent, const u32* perm, const u64* cnt_b,
     }
 }
 
-// Kept-root flags (input of the id scan), after every size is final.
-__global__ void k_sorted_flags(const u32* parent, const u32* size, const u64* n_sig_p, u64 mu,
-                               u32* flag, Counters* ctr) {
+// Kept-root flag of sorted position i (root with >= mu tiles), evaluated
+// inside the id scan: the root of a component is its smallest tile, so the
+// exclusive scan of the flags in sorted order is the canonical id
+// (finalize_clusters agglomerate.hpp:186-190).
+struct KeptRoot {
+    const u32* parent;
+    const u32* size;
+    u64 mu;
+    __host__ __device__ u32 operator()(u32 i) const { return parent[i] == i && size[i] >= mu; }
+};
+using KeptIter = thrust::transform_iterator<KeptRoot, thrust::counting_iterator<u32>>;
+
+
+// Canonical ids: id of a tile = scan value at its root (when the root is
+// kept); scattered to bucket order for the labelling pass; cluster k's root
+// recorded for cluster facts; roots counted.
+__global__ void k_sorted_label(const u32* parent, const u32* size, u64 mu, const u32* scan,
+                               const u32* perm, const u64* n_sig_p, int* tile_cid_b,
+                               int* cid_s, u32* clu_root, Counters* ctr) {
     const u64 n = *n_sig_p;
     u32 roots = 0;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x) {
-        const bool root = parent[i] == (u32)i;
-        roots += root;
-        flag[i] = (root && size[i] >= mu) ? 1u : 0u;
+        const u32 r = parent[i];
+        const bool kept = size[r] >= mu;
+        const int cid = kept ? (int)scan[r] : -1;
+        cid_s[i] = cid;
+        tile_cid_b[perm[i]] = cid;
+        if (r == (u32)i) {
+            ++roots;
+            if (kept) clu_root[cid] = (u32)i;
+        }
+        if (i == n - 1) ctr->n_kept = (u64)scan[i] + (r == (u32)i && kept ? 1u : 0u);
     }
     const u32 w = __reduce_add_sync(kFull, roots);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(&ctr->n_roots, (u64)w);
-}
-
-// Canonical ids: id of a tile = scan value at its root; scattered to bucket
-// order for the labelling pass; cluster k's root recorded for cluster facts.
-__global__ void k_sorted_label(const u32* parent, const u32* flag, const u32* scan,
-                               const u32* perm, const u64* n_sig_p, int* tile_cid_b,
-                               int* cid_s, u32* clu_root, Counters* ctr) {
-    const u64 n = *n_sig_p;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x) {
-        const u32 r = parent[i];
-        const int cid = flag[r] ? (int)scan[r] : -1;
-        cid_s[i] = cid;
-        tile_cid_b[perm[i]] = cid;
-        if (r == (u32)i && cid >= 0) clu_root[cid] = (u32)i;
-        if (i == n - 1) ctr->n_kept = (u64)scan[i] + flag[i];
-    }
 }
 
 // Key sort by columns (when the column field has <= kColBitsMax bits): a
@@ -513,6 +521,12 @@ size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x) {
     cub::DeviceRadixSort::SortPairs((void*)nullptr, a, (const u64*)nullptr, (u64*)nullptr,
                                     (const u32*)nullptr, (u32*)nullptr, (int)n, 0, bits);
     cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const u32*)nullptr, (u32*)nullptr, (int)n);
+    {
+        size_t b2 = 0;
+        const KeptIter kept(thrust::counting_iterator<u32>(0), KeptRoot{nullptr, nullptr, 0});
+        cub::DeviceScan::ExclusiveSum((void*)nullptr, b2, kept, (u32*)nullptr, (int)n);
+        b = std::max(b, b2);
+    }
     const u64 cols = sorted_columns(bits_x);
     if (cols) {
         cub::DeviceScan::ExclusiveSum((void*)nullptr, c, (const u32*)nullptr, (u32*)nullptr,
@@ -586,11 +600,11 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
     k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size, L.npts,
                                         L.flag, L.mu);
-    k_sorted_flags<<<gs, 256, 0, st>>>(L.parent, L.size, L.n_sig_dev, L.mu, L.flag, L.ctr);
     bytes = L.temp_bytes;
-    e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.flag, L.scan, (int)n, st);
+    const KeptIter kept(thrust::counting_iterator<u32>(0), KeptRoot{L.parent, L.size, L.mu});
+    e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, kept, L.scan, (int)n, st);
     if (e != cudaSuccess) return e;
-    k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.flag, L.scan, L.perm, L.n_sig_dev,
+    k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.size, L.mu, L.scan, L.perm, L.n_sig_dev,
                                        L.tile_cid_b, L.cid_s, L.clu_root, L.ctr);
     return cudaGetLastError();
 }
