@@ -72,6 +72,37 @@ __device__ __forceinline__ u32 l_find(volatile u32* lp, u32 x) {
     return x;
 }
 
+// Find with path halving (shared memory). Parents only ever move to smaller
+// members of the same set, so a plain store of the grandparent is safe: a
+// lost race only loses compression. Roots are never written here.
+__device__ __forceinline__ u32 l_find_h(volatile u32* lp, u32 x) {
+    u32 p = lp[x];
+    while (p != x) {
+        const u32 g = lp[p];
+        if (g == p) return p;
+        lp[x] = g;
+        x = g;
+        p = lp[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ void l_unite_h(u32* lp, u32 a, u32 b) {
+    volatile u32* v = lp;
+    u32 ra = l_find_h(v, a), rb = l_find_h(v, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 t = ra;
+            ra = rb;
+            rb = t;
+        }
+        const u32 old = atomicCAS(lp + ra, ra, rb);
+        if (old == ra) return;
+        ra = l_find_h(v, old);
+        rb = l_find_h(v, rb);
+    }
+}
+
 __device__ __forceinline__ void l_unite(u32* lp, u32 a, u32 b) {
     volatile u32* v = lp;
     u32 ra = l_find(v, a), rb = l_find(v, b);
@@ -241,7 +272,8 @@ __global__ void __launch_bounds__(256) k_sorted_union_c1(const u64* skey, const 
         if (valid) {
             const u64 k = s_key[loc];
             const u64 y = k & ymask;
-            if (i + 1 < n && key_at(i + 1) == k + 1) nb[0] = (u32)(i + 1);  // (x, y+1)
+            // (x, y+1); key + 1 wraps to (x+1, 0) when y is the top row
+            if (y != ymask && i + 1 < n && key_at(i + 1) == k + 1) nb[0] = (u32)(i + 1);
             const u64 nxk = k + (1ull << bits_y);                          // (x+1, y)
             if ((nxk >> bits_y) == (k >> bits_y) + 1) {
                 const u64 lo = y > 0 ? nxk - 1 : nxk;
@@ -508,6 +540,315 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bucketed column sort (default when every column holds <= kBktMaxCol tiles).
+//
+// The column counting sort gives every column its final range col_off[c] ..
+// col_off[c+1]. Columns are grouped into buckets of about kBkt tiles: the
+// bucket of a column is col_off[c] / kBkt, so a bucket is a run of whole
+// columns whose sorted range [rs[b], rs[b+1]) is shorter than kBkt + the
+// longest column. Then
+//   P1 k_bkt_scatter: each block ranks its 8192 keys per bucket in shared
+//      memory and reserves one range per (block, bucket) — about one global
+//      atomic per two keys instead of one per column group of a warp;
+//   P2 k_bkt_sort: one block per bucket places the bucket's keys by column in
+//      shared memory, ranks each key inside its (short) column, writes the
+//      sorted run, and (Chebyshev delta 1) resolves the bucket's unions in a
+//      shared-memory union-find — the whole bucket is the union window;
+//   P3 k_bkt_cross: the only edges P2 cannot see join the last column of a
+//      bucket and the first column of the next; one warp per bucket boundary
+//      unites them in the global union-find.
+// Every component's root is its smallest sorted index, as in the 256-tile
+// window kernels, so the reduce / id / label passes are shared.
+// ---------------------------------------------------------------------------
+constexpr u32 kBktShift = 12;
+constexpr u32 kBkt = 1u << kBktShift;  // tiles per bucket (target)
+constexpr int kP1Threads = 512;
+constexpr int kP1Per = 16;              // keys per thread: 8192 per block
+constexpr u32 kP1Tile = kP1Threads * kP1Per;
+constexpr u32 kP1RankBits = 13;         // rank inside a block's tile < 8192
+constexpr int kP2Threads = 512;
+constexpr int kP2Items = 12;            // bucket capacity <= 512 * 12 = 6144
+constexpr u32 kP2Cap = kP2Threads * kP2Items;
+#ifndef RG_BKT_MAX_COL
+#define RG_BKT_MAX_COL 2048
+#endif
+constexpr u64 kBktMaxCol = RG_BKT_MAX_COL;  // kBkt + kBktMaxCol <= kP2Cap
+
+// rs[b] = first column start >= b * kBkt (lower bound in col_off), rs[nbkt] = n;
+// the scatter cursors start there.
+__global__ void k_bkt_bounds(const u32* col_off, u64 cols, u64 n, u32 nbkt, u32* rs, u32* cur) {
+    for (u64 b = blockIdx.x * (u64)blockDim.x + threadIdx.x; b <= nbkt;
+         b += (u64)gridDim.x * blockDim.x) {
+        u32 v = (u32)n;
+        if (b < nbkt) {
+            const u64 target = b << kBktShift;
+            u64 lo = 0, hi = cols + 1;  // col_off has cols + 1 entries, col_off[cols] = n
+            while (lo < hi) {
+                const u64 m = (lo + hi) >> 1;
+                if ((u64)col_off[m] < target) lo = m + 1;
+                else hi = m;
+            }
+            v = lo <= cols ? col_off[lo] : (u32)n;
+            cur[b] = v;
+        }
+        rs[b] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 n, u32 bits_y,
+                                                            const u32* col_off, u32* cur,
+                                                            u32 nbkt, u64* k_out, u32* v_out) {
+    extern __shared__ u32 sh_p1[];
+    u32* hist = sh_p1;
+    u32* base = sh_p1 + nbkt;
+    for (u64 t0 = blockIdx.x * (u64)kP1Tile; t0 < n; t0 += (u64)gridDim.x * kP1Tile) {
+        for (u32 b = threadIdx.x; b < nbkt; b += kP1Threads) hist[b] = 0;
+        __syncthreads();
+        u64 k[kP1Per];
+        u32 br[kP1Per];
+#pragma unroll
+        for (int j = 0; j < kP1Per; ++j) {
+            const u64 i = t0 + (u64)j * kP1Threads + threadIdx.x;
+            k[j] = i < n ? key[i] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kP1Per; ++j) {
+            const u64 i = t0 + (u64)j * kP1Threads + threadIdx.x;
+            br[j] = 0xffffffffu;
+            if (i < n) {
+                const u32 b = __ldg(col_off + (k[j] >> bits_y)) >> kBktShift;
+                br[j] = (b << kP1RankBits) | atomicAdd(&hist[b], 1u);
+            }
+        }
+        __syncthreads();
+        for (u32 b = threadIdx.x; b < nbkt; b += kP1Threads) {
+            const u32 c = hist[b];
+            if (c) base[b] = atomicAdd(cur + b, c);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kP1Per; ++j) {
+            if (br[j] != 0xffffffffu) {
+                const u32 pos = base[br[j] >> kP1RankBits] + (br[j] & ((1u << kP1RankBits) - 1));
+                k_out[pos] = k[j];
+                v_out[pos] = (u32)(t0 + (u64)j * kP1Threads + threadIdx.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Shared memory per P2 block: keys, perm, a per-slot u32 (column cursor /
+// column length, then union-find parent) and the slot's column start (u16).
+constexpr size_t kP2Smem = (size_t)kP2Cap * (8 + 4 + 4 + 2);
+
+template <bool kUnion>
+__global__ void __launch_bounds__(kP2Threads, 2) k_bkt_sort(const u64* kin, const u32* vin,
+                                                            const u32* rs, u32 nbkt,
+                                                            const u32* col_off, u32 bits_y,
+                                                            u64* skey, u32* perm, u32* parent,
+                                                            u32* size, u64* npts) {
+    extern __shared__ u64 sh_p2[];
+    u64* sk = sh_p2;
+    u32* sp = (u32*)(sk + kP2Cap);
+    u32* aux = sp + kP2Cap;
+    unsigned short* cst = (unsigned short*)(aux + kP2Cap);
+    const u32 tid = threadIdx.x;
+    for (u32 b = blockIdx.x; b < nbkt; b += gridDim.x) {
+        const u32 r0 = rs[b], r1 = rs[b + 1];
+        const u32 m = r1 - r0;
+        for (u32 j = tid; j < m; j += kP2Threads) aux[j] = 0;
+        // all of this thread's keys, perms and column starts in flight together
+        u64 kk[kP2Items];
+        u32 pp[kP2Items], cs[kP2Items];
+#pragma unroll
+        for (int q = 0; q < kP2Items; ++q) {
+            const u32 j = tid + q * kP2Threads;
+            if (j < m) {
+                kk[q] = kin[r0 + j];
+                pp[q] = vin[r0 + j];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kP2Items; ++q) {
+            const u32 j = tid + q * kP2Threads;
+            if (j < m) cs[q] = __ldg(col_off + (kk[q] >> bits_y)) - r0;
+        }
+        __syncthreads();
+        // place by column (order inside a column arbitrary); the cursor ends
+        // as the column's length
+#pragma unroll
+        for (int q = 0; q < kP2Items; ++q) {
+            const u32 j = tid + q * kP2Threads;
+            if (j < m) {
+                const u32 slot = cs[q] + atomicAdd(&aux[cs[q]], 1u);
+                sk[slot] = kk[q];
+                sp[slot] = pp[q];
+                cst[slot] = (unsigned short)cs[q];
+            }
+        }
+        __syncthreads();
+        // rank inside the column (columns are short: at most kBktMaxCol);
+        // rows compared as u32 words, four per step
+#pragma unroll
+        for (int q = 0; q < kP2Items; ++q) {
+            const u32 j = tid + q * kP2Threads;
+            if (j < m) {
+                const u64 k = sk[j];
+                const u32 s = cst[j], e = s + aux[s];
+                u32 rank = 0;
+                if (bits_y <= 32) {
+                    const u32* lo = reinterpret_cast<const u32*>(sk);
+                    const u32 y = (u32)k;
+                    u32 t = s;
+                    for (; t + 4 <= e; t += 4)
+                        rank += (lo[2 * t] < y) + (lo[2 * t + 2] < y) + (lo[2 * t + 4] < y) +
+                                (lo[2 * t + 6] < y);
+                    for (; t < e; ++t) rank += lo[2 * t] < y;
+                } else {
+                    for (u32 t = s; t < e; ++t) rank += sk[t] < k;
+                }
+                kk[q] = k;
+                pp[q] = sp[j];
+                cs[q] = s + rank;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kP2Items; ++q) {
+            const u32 j = tid + q * kP2Threads;
+            if (j < m) {
+                sk[cs[q]] = kk[q];
+                sp[cs[q]] = pp[q];  // cst[] is unchanged: same column
+            }
+        }
+        __syncthreads();
+        for (u32 j = tid; j < m; j += kP2Threads) {
+            skey[r0 + j] = sk[j];
+            perm[r0 + j] = sp[j];
+        }
+        if (kUnion) {
+            __syncthreads();
+            // Chebyshev delta 1 inside the bucket: (x, y+1) is the next
+            // entry of the same column; column x+1, when it is in this
+            // bucket, is the run right after column x. Diagonals made
+            // redundant by an orthogonal neighbour are skipped (see
+            // k_sorted_union_c1), which leaves at most two forward partners
+            // per tile. Partners are found first (the searches stay
+            // converged) and packed into sp: two 16-bit local indices,
+            // 0xffff = none. Column x+1 in the next bucket is P3's.
+            // A vertical run (consecutive rows of one column) is one set from
+            // the start: every tile's initial parent is its run's first
+            // tile, so only the horizontal / diagonal edges need unions.
+            for (u32 j = tid; j < m; j += kP2Threads) {
+                const u64 k = sk[j];
+                const u32 s = cst[j], e = s + aux[s];
+                const bool up = j + 1 < e && sk[j + 1] == k + 1;
+                u32 h = j;
+                while (h > s && sk[h - 1] == sk[h] - 1) --h;
+                u32 pa = 0xffffu, pb = 0xffffu;
+                const u64 nxk = k + (1ull << bits_y);
+                if (e < m && (sk[e] >> bits_y) == (nxk >> bits_y)) {
+                    const u32 ne = e + aux[e];
+                    const u64 y = k & ((1ull << bits_y) - 1);
+                    const u64 lo = y > 0 ? nxk - 1 : nxk;
+                    u32 a = e, bb = ne;
+                    while (a < bb) {
+                        const u32 mid = (a + bb) >> 1;
+                        if (sk[mid] < lo) a = mid + 1;
+                        else bb = mid;
+                    }
+                    u32 dm = 0xffffu, d0 = 0xffffu, dp = 0xffffu;
+                    const u32 stop = min(ne, a + 3);
+                    for (u32 t = a; t < stop; ++t) {
+                        const u64 kt = sk[t];
+                        if (kt == nxk - 1 && y > 0) dm = t;
+                        else if (kt == nxk) d0 = t;
+                        else if (kt == nxk + 1) dp = t;
+                    }
+                    if (d0 != 0xffffu) {
+                        if (pa == 0xffffu) pa = d0;
+                        else pb = d0;
+                    } else {
+                        if (dm != 0xffffu) {
+                            if (pa == 0xffffu) pa = dm;
+                            else pb = dm;
+                        }
+                        if (dp != 0xffffu && !up) {
+                            if (pa == 0xffffu) pa = dp;
+                            else pb = dp;
+                        }
+                    }
+                }
+                sp[j] = pa | (pb << 16);
+                cst[j] = (unsigned short)h;  // only this thread reads cst[j] here
+            }
+            __syncthreads();
+            for (u32 j = tid; j < m; j += kP2Threads) aux[j] = cst[j];
+            __syncthreads();
+            // warp-uniform trip counts with a reconvergence point per
+            // round: divergent find loops must not split the warp for the
+            // rest of the bucket
+            for (u32 j0 = 0; j0 < m; j0 += kP2Threads) {
+                const u32 j = j0 + tid;
+                if (j < m) {
+                    const u32 e = sp[j];
+                    if ((e & 0xffffu) != 0xffffu) l_unite_h(aux, j, e & 0xffffu);
+                    if ((e >> 16) != 0xffffu) l_unite_h(aux, j, e >> 16);
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            for (u32 j0 = 0; j0 < m; j0 += kP2Threads) {
+                const u32 j = j0 + tid;
+                if (j < m) {
+                    parent[r0 + j] = r0 + l_find_h(aux, j);
+                    size[r0 + j] = 0;
+                    npts[r0 + j] = 0;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Edges between the last column of bucket b and the first column of bucket
+// b+1 (Chebyshev delta 1, all three offsets; no elision needed).
+__global__ void k_bkt_cross(const u64* skey, const u32* rs, u32 nbkt, const u32* col_off,
+                            u64 cols, u32 bits_y, u32* parent) {
+    const int lane = threadIdx.x & 31;
+    const u64 ymask = (1ull << bits_y) - 1;
+    const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+    const u64 n_warps = ((u64)gridDim.x * blockDim.x) >> 5;
+    for (u64 b = warp; b + 1 < nbkt; b += n_warps) {
+        const u32 re = rs[b + 1];
+        if (re == rs[b]) continue;
+        const u64 xl = skey[re - 1] >> bits_y;
+        if (xl + 1 >= cols) continue;
+        const u32 ns = col_off[xl + 1], ne = col_off[xl + 2];
+        if (ne == ns) continue;  // column x+1 empty
+        for (u32 t = col_off[xl] + lane; t < re; t += 32) {
+            const u64 k = skey[t];
+            const u64 y = k & ymask;
+            const u64 nxk = k + (1ull << bits_y);
+            const u64 lo = y > 0 ? nxk - 1 : nxk;
+            u32 a = ns, bb = ne;
+            while (a < bb) {
+                const u32 mid = (a + bb) >> 1;
+                if (skey[mid] < lo) a = mid + 1;
+                else bb = mid;
+            }
+            for (u32 q = a; q < ne; ++q) {
+                const u64 kq = skey[q];
+                if (kq > nxk + 1 || (kq == nxk + 1 && y == ymask)) break;
+                s_unite(parent, t, q);
+            }
+        }
+    }
+}
+
 static int grid_for_s(u64 n, int n_sm, int per_sm) {
     const u64 want = (n + 255) / 256;
     const u64 cap = (u64)n_sm * per_sm;
@@ -569,35 +910,99 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     if (std::getenv("RG_DEBUG"))
         std::fprintf(stderr, "[rg] K3 sorted: n=%llu max_col=%llu\n", (unsigned long long)n,
                      (unsigned long long)L.host_ctr->max_col);
-    if (n == 0) return cudaSuccess;
+    if (n == 0) {
+        if (L.launches) *L.launches = cols && L.col_cnt ? 1 : 0;
+        return cudaSuccess;
+    }
     const int gs = grid_for_s(n, L.n_sm, 16);
-    if (cols && L.col_cnt && L.host_ctr->max_col <= kSegSortMaxColumn) {
+    int launches = cols && L.col_cnt ? 1 : 0;  // kernels launched (col_hist)
+    const u32 nbkt = (u32)((n + kBkt - 1) >> kBktShift);
+    const bool c1 = L.delta == 1 && !L.manhattan;
+    static const int variant = [] {
+        const char* v = std::getenv("RG_K3_SORT");
+        return v && v[0] == 's' ? 1 : (v && v[0] == 'r' ? 2 : 0);
+    }();
+    if (cols && L.col_cnt && variant == 0 && L.host_ctr->max_col <= kBktMaxCol &&
+        (size_t)nbkt * 8 <= 96 * 1024) {  // L.flag holds >= 1024 and >= n entries
+        // bucketed column sort (+ fused bucket-local unions for Chebyshev 1)
         e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
         if (e != cudaSuccess) return e;
-        cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32), cudaMemcpyDeviceToDevice,
-                        st);
-        k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
-                                          L.iota);
-        bytes = L.temp_bytes;
-        e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
-                                                (int)n, (int)cols, L.col_off, L.col_off + 1, st);
-        if (e != cudaSuccess) return e;
+        u32* rs = L.flag;  // nbkt + 1 region starts, then nbkt scatter cursors
+        u32* cur = L.flag + nbkt + 1;
+        k_bkt_bounds<<<(nbkt + 256) / 256, 256, 0, st>>>(L.col_off, cols, n, nbkt, rs, cur);
+        const size_t sm1 = (size_t)nbkt * 2 * sizeof(u32);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024 + 1024);
+            cudaFuncSetAttribute(k_bkt_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kP2Smem);
+            cudaFuncSetAttribute(k_bkt_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kP2Smem);
+            attr = true;
+        }
+        const u64 t1 = (n + kP1Tile - 1) / kP1Tile;
+        const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * 4);
+        k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, n, L.bits_y, L.col_off, cur, nbkt,
+                                                   L.ktmp, L.iota);
+        const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * 2);
+        if (c1) {
+            k_bkt_sort<true><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
+                                                              L.bits_y, L.skey, L.perm, L.parent,
+                                                              L.size, L.npts);
+            if (nbkt > 1)
+                k_bkt_cross<<<(int)std::min<u64>((nbkt + 7) / 8, (u64)L.n_sm * 8), 256, 0, st>>>(
+                    L.skey, rs, nbkt, L.col_off, cols, L.bits_y, L.parent);
+            launches += 6;  // scan (2), bounds, scatter, sort, cross
+        } else {
+            k_bkt_sort<false><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
+                                                               L.bits_y, L.skey, L.perm, L.parent,
+                                                               L.size, L.npts);
+            launches += 5;
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (!c1) {
+            SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
+            cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
+            k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta,
+                                               L.manhattan, L.parent, L.size, L.npts, el);
+            k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
+            launches += 2;
+        }
     } else {
-        e = launch_iota(L.iota, n, L.n_sm, st);
-        if (e != cudaSuccess) return e;
-        e = cub::DeviceRadixSort::SortPairs(L.temp, bytes, L.sig_key, L.skey, L.iota, L.perm,
-                                            (int)n, 0, (int)L.key_bits, st);
-        if (e != cudaSuccess) return e;
+        if (cols && L.col_cnt && variant != 2 && L.host_ctr->max_col <= kSegSortMaxColumn) {
+            e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1),
+                                              st);
+            if (e != cudaSuccess) return e;
+            cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32),
+                            cudaMemcpyDeviceToDevice, st);
+            k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
+                                              L.iota);
+            bytes = L.temp_bytes;
+            e = cub::DeviceSegmentedSort::SortPairs(L.temp, bytes, L.ktmp, L.skey, L.iota, L.perm,
+                                                    (int)n, (int)cols, L.col_off, L.col_off + 1,
+                                                    st);
+            if (e != cudaSuccess) return e;
+            launches += 7;  // scan (2), scatter, segmented sort (4)
+        } else {
+            e = launch_iota(L.iota, n, L.n_sm, st);
+            if (e != cudaSuccess) return e;
+            e = cub::DeviceRadixSort::SortPairs(L.temp, bytes, L.sig_key, L.skey, L.iota, L.perm,
+                                                (int)n, 0, (int)L.key_bits, st);
+            if (e != cudaSuccess) return e;
+            launches += 1 + 2 * (((int)L.key_bits + 7) / 8) + 1;  // iota + onesweep passes
+        }
+        SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
+        cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
+        if (c1)
+            k_sorted_union_c1<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.parent, L.size,
+                                                  L.npts, el);
+        else
+            k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta,
+                                               L.manhattan, L.parent, L.size, L.npts, el);
+        k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
+        launches += 2;
     }
-    SortedEdges el{L.edges, L.edge_cap, &L.ctr->n_edges};
-    cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
-    if (L.delta == 1 && !L.manhattan)
-        k_sorted_union_c1<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.parent, L.size,
-                                              L.npts, el);
-    else
-        k_sorted_union<<<gs, 256, 0, st>>>(L.skey, L.n_sig_dev, L.bits_y, L.delta, L.manhattan,
-                                           L.parent, L.size, L.npts, el);
-    k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
     k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size, L.npts,
                                         L.flag, L.mu);
     bytes = L.temp_bytes;
@@ -606,6 +1011,8 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.size, L.mu, L.scan, L.perm, L.n_sig_dev,
                                        L.tile_cid_b, L.cid_s, L.clu_root, L.ctr);
+    launches += 4;  // reduce, scan (2), label
+    if (L.launches) *L.launches = launches;
     return cudaGetLastError();
 }
 

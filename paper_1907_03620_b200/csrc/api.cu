@@ -908,8 +908,10 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     L.n_sm = ctx->n_sm;
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);
+    int launched = 0;
+    L.launches = &launched;
     CK(launch_agglomerate_sorted(L, ctx->st));
-    ctx->launches += 14;  // iota + radix sort (6) + union, edges, reduce, flags, scan (2), label
+    ctx->launches += launched;
     if (fused) return RG_OK;
     CK(cudaMemcpyAsync(&ctx->hctr->n_roots, &ctx->ctr->n_roots, 2 * sizeof(u64),
                        cudaMemcpyDeviceToHost, ctx->st));

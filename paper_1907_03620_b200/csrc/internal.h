@@ -102,6 +102,7 @@ struct SortedLaunch {
     Counters* ctr;
     Counters* host_ctr;   // pinned mirror: the exact count is read back once
     int n_sm;
+    int* launches;        // out: kernels launched
 };
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
 u64 sorted_columns(u32 bits_x);

@@ -285,3 +285,28 @@ def test_dense_cluster_yields_a_significant_tile():
     acc = TileAccumulator(gp)
     acc.ingest(pts)
     assert len(acc.prune()) >= 1
+
+
+@pytest.mark.parametrize("k3", ["bucket", "seg", "radix"])
+def test_top_row_key_wrap_is_not_adjacency(monkeypatch, k3):
+    """With a row range of exactly 2^bits_y rows, the packed key of (x, top
+    row) + 1 is the key of (x+1, bottom row): consecutive in sorted order but
+    not adjacent (agglomerate.hpp:38-50 offsets are geometric). Off-canvas
+    tile sets get a key packing sized to their own extent, so 4 rows -> 2
+    row bits; every sort path of the sorted K3 must keep them apart."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "from paper_1907_03620_b200.raster import GridParams, Tile, agglomerate_flat\n"
+        "gp = GridParams(precision=2, min_cluster_size=1)\n"
+        "b = 10**12\n"
+        "t = {Tile(b, 0): 5, Tile(b, 3): 5, Tile(b + 1, 0): 5, Tile(b + 2, 3): 5, Tile(b + 3, 0): 5}\n"
+        "f = agglomerate_flat(t, gp)\n"
+        "print(f.n_clusters, f.cluster_id.tolist())\n")
+    env = dict(os.environ, RG_K3_SORT=k3[0])
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         check=True).stdout.split("\n")[0]
+    # (b,0)-(b+1,0) adjacent; (b,3) alone; (b+2,3) alone; (b+3,0) alone
+    assert out == "4 [0, 1, 0, 2, 3]", out
