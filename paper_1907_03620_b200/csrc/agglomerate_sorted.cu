@@ -497,6 +497,15 @@ __global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt,
     if (lane == 0 && mx) atomicMax(max_col, mx);
 }
 
+__global__ void k_col_max(const u32* cnt, u64 cols, u32* max_col) {
+    u32 mx = 0;
+    for (u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x; c < cols;
+         c += (u64)gridDim.x * blockDim.x)
+        mx = max(mx, cnt[c]);
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_col, mx);
+}
+
 // Each thread scatters kColIlp keys of a warp tile whose reservations are in
 // flight together (the reservation's round trip, not bandwidth, bounds a
 // one-key-per-iteration scatter).
@@ -894,10 +903,15 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     size_t bytes = L.temp_bytes;
     const u64 cols = sorted_columns(L.key_bits - L.bits_y);
     if (cols && L.col_cnt) {
-        cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
         cudaMemsetAsync(&L.ctr->max_col, 0, sizeof(u64), st);
-        k_col_hist<<<grid_for_s(L.n_sig, L.n_sm, 16), 256, 0, st>>>(
-            L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, (u32*)&L.ctr->max_col);
+        if (L.col_hist_ready) {  // K2 built the histogram; only its maximum is missing
+            const int g = (int)std::min<u64>((cols + 255) / 256, (u64)L.n_sm * 8);
+            k_col_max<<<g, 256, 0, st>>>(L.col_cnt, cols, (u32*)&L.ctr->max_col);
+        } else {
+            cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
+            k_col_hist<<<grid_for_s(L.n_sig, L.n_sm, 16), 256, 0, st>>>(
+                L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, (u32*)&L.ctr->max_col);
+        }
     }
     // The exact significant count (L.n_sig may be an upper bound) and the
     // longest column decide the sort and size every launch below.

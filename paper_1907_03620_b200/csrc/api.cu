@@ -194,6 +194,7 @@ struct rg_ctx {
     u64 s_cap = 0, s_edge_cap = 0;
     u32 *s_col_cnt = nullptr, *s_col_off = nullptr;
     u64 s_cols = 0;
+    bool col_hist_ready = false;  // s_col_cnt holds the histogram of the current sig set (K2)
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -417,6 +418,7 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
     }
     ctx->ps_used = 0;
     ctx->used = 0;
+    ctx->col_hist_ready = false;
     ctx->table_dirty = false;
     ctx->state = rg_ctx::kAccum;
     ctx->n_sig = 0;
@@ -774,6 +776,17 @@ bool use_sorted_k3(const rg_ctx* ctx) {
     return ctx->p.distance <= 2 && ctx->used < 0x7fffffffull;  // S <= D = used
 }
 
+rg_status ensure_col_arrays(rg_ctx* ctx, u64 cols) {
+    if (ctx->s_cols >= cols) return RG_OK;
+    dfree(ctx->s_col_cnt);
+    dfree(ctx->s_col_off);
+    ctx->s_cols = 0;
+    CK(dalloc(&ctx->s_col_cnt, cols + 1));
+    CK(dalloc(&ctx->s_col_off, cols + 1));
+    ctx->s_cols = cols;
+    return RG_OK;
+}
+
 // K2 (+ window_fix / dedupe pre-passes) enqueued on the stream; the
 // significant count stays on the device (ctr->n_sig).
 rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
@@ -804,11 +817,20 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
             CK(launch_dedupe_counts(table_of(ctx), ctx->cap, ut_table(ctx), ctx->n_sm, ctx->st));
             ++ctx->launches;
         }
+        // the sorted K3's column histogram is built by K2 itself
+        const u64 cols = hash_k3 ? 0 : sorted_columns(ctx->grid.bits_x);
+        if (cols) {
+            s = ensure_col_arrays(ctx, cols);
+            if (s != RG_OK) return s;
+            CK(cudaMemsetAsync(ctx->s_col_cnt, 0, (cols + 1) * sizeof(u32), ctx->st));
+        }
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
                           window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
                           ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
-                          ctx->root_cid, ctx->ctr, ctx->n_sm, ctx->st));
+                          ctx->root_cid, cols ? ctx->s_col_cnt : nullptr, ctx->ctr, ctx->n_sm,
+                          ctx->st));
         ++ctx->launches;
+        ctx->col_hist_ready = cols != 0;
     }
     return RG_OK;
 }
@@ -860,13 +882,9 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
         ctx->s_edge_cap = ecap;
     }
     const u64 cols = sorted_columns(ctx->res.bits_x);
-    if (cols && ctx->s_cols < cols) {
-        dfree(ctx->s_col_cnt);
-        dfree(ctx->s_col_off);
-        ctx->s_cols = 0;
-        CK(dalloc(&ctx->s_col_cnt, cols + 1));
-        CK(dalloc(&ctx->s_col_off, cols + 1));
-        ctx->s_cols = cols;
+    if (cols) {
+        rg_status s = ensure_col_arrays(ctx, cols);
+        if (s != RG_OK) return s;
     }
     const size_t tb = sorted_temp_bytes(n, kb, ctx->res.bits_x);
     if (ctx->sort_temp_bytes < tb || !ctx->sort_temp) {
@@ -906,6 +924,9 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     L.ctr = ctx->ctr;
     L.host_ctr = ctx->hctr;
     L.n_sm = ctx->n_sm;
+    // K2's histogram is valid for the set it compacted (canvas packing)
+    L.col_hist_ready = ctx->col_hist_ready;
+    ctx->col_hist_ready = false;  // one use: the segmented-sort path consumes col_cnt
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);
     int launched = 0;
@@ -1630,6 +1651,7 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     ctx->n_sig = n;
     ctx->res = res;
     ctx->res_is_canvas = on_canvas;
+    ctx->col_hist_ready = false;
     ctx->state = rg_ctx::kSig;
     ctx->sorted = false;
     ctx->table_dirty = true;

@@ -135,6 +135,10 @@ __device__ __forceinline__ void red_add(u64* p, u64 v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_add_u32(u32* p, u32 v) {
+    asm volatile("red.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Streaming 128-bit load of one point (read once: keep it out of L1 and
 // mark it evict-first in L2 so the hash table stays resident).
 __device__ __forceinline__ u64 evict_first_policy() {

@@ -586,6 +586,8 @@ struct K2Out {
     u64* npts;
     u64* min_key;
     int* root_cid;
+    u32* col_cnt;  // sorted K3: per-column tile counts (key >> bits_y), or null
+    u32 bits_y;
 };
 
 __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n, const K2Out& o,
@@ -608,6 +610,18 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
             o.root_cid[pos] = -1;
         }
         t.slots[i].count = kSigBit | pos;
+    }
+    if (o.col_cnt) {
+        // column histogram of the sorted K3 (replaces its k_col_hist pass):
+        // flushed slots come in table order, so a warp's keys share a few
+        // 4x4 blocks and columns; one RED per distinct column of a warp
+        for (u32 e0 = 0; e0 < n; e0 += 32) {
+            const u32 e = e0 + lane;
+            const u32 col = e < n ? (u32)(o.sig_key[at + e] >> o.bits_y) : 0xffffffffu;
+            const u32 peers = __match_any_sync(kFull, col);
+            if (col != 0xffffffffu && lane == __ffs(peers) - 1)
+                red_add_u32(o.col_cnt + col, (u32)__popc(peers));
+        }
     }
     __syncwarp();
 }
@@ -777,7 +791,7 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
-                           Counters* ctr, int n_sm, cudaStream_t st) {
+                           u32* col_cnt, Counters* ctr, int n_sm, cudaStream_t st) {
 #ifndef RG_K2_BPS
 #define RG_K2_BPS 16
 #endif
@@ -785,7 +799,7 @@ cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_k
     const u64 want = (cap + per_block - 1) / per_block;
     const u64 mx = (u64)n_sm * RG_K2_BPS;
     const int blocks = (int)(want < mx ? (want ? want : 1) : mx);
-    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid};
+    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid, col_cnt, t.bits_y};
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, keep, o, ctr);
     return cudaGetLastError();
 }

@@ -37,7 +37,7 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
-                           Counters* ctr, int n_sm, cudaStream_t st);
+                           u32* col_cnt, Counters* ctr, int n_sm, cudaStream_t st);
 cudaError_t launch_window_mark(Table t, u64 cap, u64 tau, u32 bits_x, u8* keep, int n_sm,
                                cudaStream_t st);
 
@@ -102,6 +102,7 @@ struct SortedLaunch {
     Counters* ctr;
     Counters* host_ctr;   // pinned mirror: the exact count is read back once
     int n_sm;
+    bool col_hist_ready;  // K2 already built col_cnt (prune_enqueue)
     int* launches;        // out: kernels launched
 };
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
