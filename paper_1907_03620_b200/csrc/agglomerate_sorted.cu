@@ -66,6 +66,26 @@ __device__ __forceinline__ void s_unite(u32* parent, u32 a, u32 b) {
     }
 }
 
+// s_unite that records the root it links under another (each root is
+// linked at most once), so its counts can be folded into the final root.
+__device__ __forceinline__ void s_unite_rec(u32* parent, u32 a, u32 b, u32* linked,
+                                            u64* n_linked) {
+    u32 ra = s_find(parent, a), rb = s_find(parent, b);
+    while (ra != rb) {
+        if (ra < rb) {
+            const u32 t = ra;
+            ra = rb;
+            rb = t;
+        }
+        const u32 old = atomicCAS(parent + ra, ra, rb);
+        if (old == ra) {
+            linked[atomicAdd(n_linked, 1ull)] = ra;
+            return;
+        }
+        ra = old;
+    }
+}
+
 __device__ __forceinline__ u32 l_find(volatile u32* lp, u32 x) {
     u32 p;
     while ((p = lp[x]) != x) x = p;
@@ -452,7 +472,8 @@ __global__ void k_sorted_label(const u32* parent, const u32* size, u64 mu, const
     u32 roots = 0;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x) {
-        const u32 r = parent[i];
+        u32 r = parent[i], nx;
+        while ((nx = s_ld_parent(parent + r)) != r) r = nx;  // linked bucket roots (P3)
         const bool kept = size[r] >= mu;
         const int cid = kept ? (int)scan[r] : -1;
         cid_s[i] = cid;
@@ -656,8 +677,9 @@ template <bool kUnion>
 __global__ void __launch_bounds__(kP2Threads, 2) k_bkt_sort(const u64* kin, const u32* vin,
                                                             const u32* rs, u32 nbkt,
                                                             const u32* col_off, u32 bits_y,
-                                                            u64* skey, u32* perm, u32* parent,
-                                                            u32* size, u64* npts) {
+                                                            const u64* cnt_b, u64* skey,
+                                                            u32* perm, u32* parent, u32* size,
+                                                            u64* npts) {
     extern __shared__ u64 sh_p2[];
     u64* sk = sh_p2;
     u32* sp = (u32*)(sk + kP2Cap);
@@ -809,15 +831,24 @@ __global__ void __launch_bounds__(kP2Threads, 2) k_bkt_sort(const u64* kin, cons
                 __syncwarp();
             }
             __syncthreads();
+            // flatten; tiles per bucket-local root (sp is free now: perm is
+            // written, partners consumed). Points per cluster are not part of
+            // the clustering (Cluster agglomerate.hpp:18-23 has none): they
+            // are summed on demand by rg_get_clusters.
+            for (u32 j = tid; j < m; j += kP2Threads) sp[j] = 0;
+            __syncthreads();
             for (u32 j0 = 0; j0 < m; j0 += kP2Threads) {
                 const u32 j = j0 + tid;
                 if (j < m) {
-                    parent[r0 + j] = r0 + l_find_h(aux, j);
-                    size[r0 + j] = 0;
-                    npts[r0 + j] = 0;
+                    const u32 r = l_find_h(aux, j);
+                    parent[r0 + j] = r0 + r;
+                    atomicAdd(&sp[r], 1u);
                 }
                 __syncwarp();
             }
+            __syncthreads();
+            for (u32 j = tid; j < m; j += kP2Threads)
+                if (aux[j] == j) size[r0 + j] = sp[j];
         }
         __syncthreads();
     }
@@ -826,7 +857,7 @@ __global__ void __launch_bounds__(kP2Threads, 2) k_bkt_sort(const u64* kin, cons
 // Edges between the last column of bucket b and the first column of bucket
 // b+1 (Chebyshev delta 1, all three offsets; no elision needed).
 __global__ void k_bkt_cross(const u64* skey, const u32* rs, u32 nbkt, const u32* col_off,
-                            u64 cols, u32 bits_y, u32* parent) {
+                            u64 cols, u32 bits_y, u32* parent, u32* linked, u64* n_linked) {
     const int lane = threadIdx.x & 31;
     const u64 ymask = (1ull << bits_y) - 1;
     const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
@@ -852,10 +883,63 @@ __global__ void k_bkt_cross(const u64* skey, const u32* rs, u32 nbkt, const u32*
             for (u32 q = a; q < ne; ++q) {
                 const u64 kq = skey[q];
                 if (kq > nxk + 1 || (kq == nxk + 1 && y == ymask)) break;
-                s_unite(parent, t, q);
+                s_unite_rec(parent, t, q, linked, n_linked);
             }
         }
     }
+}
+
+// Fold the tile count of every bucket-local root that P3 linked
+// under another root into its final root (the final root's own count is
+// already there; a linked root receives nothing, so its count is its own).
+__global__ void k_bkt_merge(const u32* linked, const u64* n_linked, u32* parent, u32* size,
+                            u64* npts) {
+    const u64 n = *n_linked;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 ra = linked[i];
+        const u32 f = s_find(parent, ra);
+        atomicAdd(size + f, size[ra]);
+    }
+}
+
+// Points per cluster on demand (after the bucketed K3, which leaves npts
+// unset): npts[root of cluster k] = sum of its tiles' counts. Runs of equal
+// ids within a warp are pre-summed.
+__global__ void k_cluster_npts(const int* cid_s, const u32* perm, const u64* cnt_b, u64 n,
+                               const u32* clu_root, u64* npts) {
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int c = i < n ? cid_s[i] : -1;
+        u64 p = c >= 0 ? cnt_b[perm[i]] : 0ull;
+        const int prev = __shfl_up_sync(kFull, c, 1);
+        const bool head = lane == 0 || prev != c;
+        const u32 heads = __ballot_sync(kFull, head);
+        const u32 run = __popc(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 orun = __shfl_down_sync(kFull, run, o);
+            const u64 op = __shfl_down_sync(kFull, p, o);
+            if (lane + o < 32 && orun == run) p += op;
+        }
+        if (head && c >= 0) atomicAdd(npts + clu_root[c], p);
+    }
+}
+
+cudaError_t launch_cluster_npts(const int* cid_s, const u32* perm, const u64* cnt_b, u64 n,
+                                const u32* clu_root, u64 n_kept, u64* npts, int n_sm,
+                                cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    // clusters' roots are sorted positions < n: clear them all
+    if ((e = cudaMemsetAsync(npts, 0, n * sizeof(u64), st)) != cudaSuccess) return e;
+    (void)n_kept;
+    if (n == 0) return cudaSuccess;
+    const u64 want = (n + 255) / 256;
+    const int g = (int)std::min<u64>(want, (u64)n_sm * 16);
+    k_cluster_npts<<<g, 256, 0, st>>>(cid_s, perm, cnt_b, n, clu_root, npts);
+    return cudaGetLastError();
 }
 
 static int grid_for_s(u64 n, int n_sm, int per_sm) {
@@ -932,6 +1016,7 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     int launches = cols && L.col_cnt ? 1 : 0;  // kernels launched (col_hist)
     const u32 nbkt = (u32)((n + kBkt - 1) >> kBktShift);
     const bool c1 = L.delta == 1 && !L.manhattan;
+    bool bucket_counts = false;  // per-root counts already final (bucketed Chebyshev-1 path)
     static const int variant = [] {
         const char* v = std::getenv("RG_K3_SORT");
         return v && v[0] == 's' ? 1 : (v && v[0] == 'r' ? 2 : 0);
@@ -962,16 +1047,25 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * 2);
         if (c1) {
             k_bkt_sort<true><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
-                                                              L.bits_y, L.skey, L.perm, L.parent,
-                                                              L.size, L.npts);
-            if (nbkt > 1)
+                                                              L.bits_y, L.sig_cnt, L.skey, L.perm,
+                                                              L.parent, L.size, L.npts);
+            launches += 5;  // scan (2), bounds, scatter, sort
+            if (nbkt > 1) {
+                u32* linked = reinterpret_cast<u32*>(L.edges);  // >= 2n u32 entries
+                cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
                 k_bkt_cross<<<(int)std::min<u64>((nbkt + 7) / 8, (u64)L.n_sm * 8), 256, 0, st>>>(
-                    L.skey, rs, nbkt, L.col_off, cols, L.bits_y, L.parent);
-            launches += 6;  // scan (2), bounds, scatter, sort, cross
+                    L.skey, rs, nbkt, L.col_off, cols, L.bits_y, L.parent, linked,
+                    &L.ctr->n_edges);
+                k_bkt_merge<<<L.n_sm, 256, 0, st>>>(linked, &L.ctr->n_edges, L.parent, L.size,
+                                                    L.npts);
+                launches += 2;
+            }
+            bucket_counts = true;
+            if (L.npts_deferred) *L.npts_deferred = true;
         } else {
             k_bkt_sort<false><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
-                                                               L.bits_y, L.skey, L.perm, L.parent,
-                                                               L.size, L.npts);
+                                                               L.bits_y, L.sig_cnt, L.skey, L.perm,
+                                                               L.parent, L.size, L.npts);
             launches += 5;
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1017,15 +1111,18 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         k_sorted_edges<<<gs, 256, 0, st>>>(el, L.parent);
         launches += 2;
     }
-    k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size, L.npts,
-                                        L.flag, L.mu);
+    if (!bucket_counts) {  // flatten + per-root counts (the bucketed union did both)
+        k_sorted_reduce<<<gs, 256, 0, st>>>(L.parent, L.perm, L.sig_cnt, L.n_sig_dev, L.size,
+                                            L.npts, L.flag, L.mu);
+        ++launches;
+    }
     bytes = L.temp_bytes;
     const KeptIter kept(thrust::counting_iterator<u32>(0), KeptRoot{L.parent, L.size, L.mu});
     e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, kept, L.scan, (int)n, st);
     if (e != cudaSuccess) return e;
     k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.size, L.mu, L.scan, L.perm, L.n_sig_dev,
                                        L.tile_cid_b, L.cid_s, L.clu_root, L.ctr);
-    launches += 4;  // reduce, scan (2), label
+    launches += 3;  // scan (2), label
     if (L.launches) *L.launches = launches;
     return cudaGetLastError();
 }

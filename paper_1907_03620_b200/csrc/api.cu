@@ -195,6 +195,7 @@ struct rg_ctx {
     u32 *s_col_cnt = nullptr, *s_col_off = nullptr;
     u64 s_cols = 0;
     bool col_hist_ready = false;  // s_col_cnt holds the histogram of the current sig set (K2)
+    bool npts_pending = false;    // sorted K3 left per-cluster point totals to rg_get_clusters
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -926,6 +927,8 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     L.n_sm = ctx->n_sm;
     // K2's histogram is valid for the set it compacted (canvas packing)
     L.col_hist_ready = ctx->col_hist_ready;
+    ctx->npts_pending = false;
+    L.npts_deferred = &ctx->npts_pending;
     ctx->col_hist_ready = false;  // one use: the segmented-sort path consumes col_cnt
     zero_field(ctx, &ctx->ctr->n_roots);
     zero_field(ctx, &ctx->ctr->n_kept);
@@ -1850,6 +1853,12 @@ rg_status rg_get_clusters(rg_ctx* ctx, uint64_t* n_tiles, uint64_t* n_points, in
         if (n_points) CK(dalloc(&dnp, w));
         if (first_tx) CK(dalloc(&dfx, w));
         if (first_ty) CK(dalloc(&dfy, w));
+    }
+    if (n_points && ctx->sorted && ctx->npts_pending) {
+        CK(launch_cluster_npts(ctx->s_cid, ctx->root_idx_sorted, ctx->sig_cnt, ctx->n_sig,
+                               ctx->s_clu_root, ctx->n_kept, ctx->npts, ctx->n_sm, ctx->st));
+        ++ctx->launches;
+        ctx->npts_pending = false;
     }
     k_cluster_facts<<<grid_for(w, ctx->n_sm), 256, 0, ctx->st>>>(
         ctx->root_key_sorted, ctx->root_idx_sorted, ctx->sorted ? ctx->s_clu_root : nullptr, w,

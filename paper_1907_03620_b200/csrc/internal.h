@@ -103,11 +103,15 @@ struct SortedLaunch {
     Counters* host_ctr;   // pinned mirror: the exact count is read back once
     int n_sm;
     bool col_hist_ready;  // K2 already built col_cnt (prune_enqueue)
+    bool* npts_deferred;  // out: per-cluster point totals left for launch_cluster_npts
     int* launches;        // out: kernels launched
 };
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
 u64 sorted_columns(u32 bits_x);
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st);
+cudaError_t launch_cluster_npts(const int* cid_s, const u32* perm, const u64* cnt_b, u64 n,
+                                const u32* clu_root, u64 n_kept, u64* npts, int n_sm,
+                                cudaStream_t st);
 cudaError_t launch_order_and_label(const AggLaunch& A, u64 n_kept, cudaStream_t st);
 size_t sort_pairs_temp_bytes(u64 n, int bits);
 cudaError_t sort_pairs(void* temp, size_t temp_bytes, const u64* k_in, u64* k_out,
