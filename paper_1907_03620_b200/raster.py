@@ -554,6 +554,21 @@ class Pipeline:
             N.RG_MEM_HOST))
         return xy, off
 
+    def cluster_facts(self):
+        """Per cluster k (canonical id order): (tiles, points, first tile x,
+        first tile y) as numpy arrays — the sizes finalize_clusters orders by
+        (agglomerate.hpp:175-191) plus the cluster's point total."""
+        n = int(self.ctx.stats().n_clusters)
+        nt = np.empty(n, np.uint64)
+        npnt = np.empty(n, np.uint64)
+        fx = np.empty(n, np.int64)
+        fy = np.empty(n, np.int64)
+        if n:
+            self.ctx.check(self.ctx.lib.rg_get_clusters(
+                self.ctx.h, nt.ctypes.data, npnt.ctypes.data, fx.ctypes.data, fy.ctypes.data, n,
+                N.RG_MEM_HOST))
+        return nt, npnt, fx, fy
+
     def launches(self) -> int:
         return int(self.ctx.lib.rg_kernel_launches(self.ctx.h))
 

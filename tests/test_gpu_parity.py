@@ -278,3 +278,43 @@ def test_config_full_size_properties(cfg):
     pl2.run(shuf)
     b = pl2.flat()
     assert_same(b, a, f"cfg{cfg} order invariance")
+
+
+@pytest.mark.parametrize("k3", ["bucket", "seg", "hash"])
+def test_cluster_facts_vs_oracle(k3):
+    """rg_get_clusters: tiles, points and smallest tile of every cluster,
+    against the oracle's flat clustering (every K3 path, incl. the bucketed
+    one whose point totals are summed on demand)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from oracle import pyoracle as O\n"
+        "from paper_1907_03620_b200 import datagen as D\n"
+        "from paper_1907_03620_b200.raster import Pipeline\n"
+        "gp = D.params(2)\n"
+        "pts = D.generate(D.spec(2, 0.3), shuffle_seed=5)\n"
+        "pl = Pipeline(gp)\n"
+        "pl.run(pts)\n"
+        "nt, npnt, fx, fy = pl.cluster_facts()\n"
+        "ref = O.port_cluster(pts, gp)\n"
+        "k = ref.cluster_id >= 0\n"
+        "c = ref.cluster_id[k]\n"
+        "assert len(nt) == ref.n_clusters > 100\n"
+        "assert np.array_equal(nt, np.bincount(c, minlength=ref.n_clusters).astype(np.uint64))\n"
+        "assert np.array_equal(npnt, np.bincount(c, weights=ref.count[k].astype(np.float64),"
+        " minlength=ref.n_clusters).astype(np.uint64))\n"
+        "first = np.full(ref.n_clusters, len(k))\n"
+        "np.minimum.at(first, c, np.nonzero(k)[0])\n"
+        "assert np.array_equal(fx, ref.tx[first]) and np.array_equal(fy, ref.ty[first])\n"
+        "print('ok')\n")
+    env = dict(os.environ)
+    if k3 == "hash":
+        env["RG_K3"] = "hash"
+    else:
+        env["RG_K3_SORT"] = k3[0]
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
