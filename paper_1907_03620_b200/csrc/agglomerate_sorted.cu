@@ -591,28 +591,30 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
 // Every component's root is its smallest sorted index, as in the 256-tile
 // window kernels, so the reduce / id / label passes are shared.
 // ---------------------------------------------------------------------------
-constexpr u32 kBktShift = 12;
-constexpr u32 kBkt = 1u << kBktShift;  // tiles per bucket (target)
+// Bucket size 2^shift tiles (host-chosen, 11 or 12) and P2 block shapes:
+// 2048-tile buckets in 256-thread blocks (55 KB, 4 blocks per SM) when
+// every column holds <= 1024 tiles, else 4096-tile buckets in 512-thread
+// blocks (108 KB, 2 per SM) for columns of <= 2048 tiles.
 constexpr int kP1Threads = 512;
 constexpr int kP1Per = 16;              // keys per thread: 8192 per block
 constexpr u32 kP1Tile = kP1Threads * kP1Per;
 constexpr u32 kP1RankBits = 13;         // rank inside a block's tile < 8192
-constexpr int kP2Threads = 512;
-constexpr int kP2Items = 12;            // bucket capacity <= 512 * 12 = 6144
-constexpr u32 kP2Cap = kP2Threads * kP2Items;
+constexpr int kP2Items = 12;
 #ifndef RG_BKT_MAX_COL
 #define RG_BKT_MAX_COL 2048
 #endif
-constexpr u64 kBktMaxCol = RG_BKT_MAX_COL;  // kBkt + kBktMaxCol <= kP2Cap
+constexpr u64 kBktMaxCol = RG_BKT_MAX_COL;  // 4096 + kBktMaxCol <= 512 * kP2Items
+constexpr size_t p2_smem(int threads) { return (size_t)threads * kP2Items * (8 + 4 + 4 + 2); }
 
 // rs[b] = first column start >= b * kBkt (lower bound in col_off), rs[nbkt] = n;
 // the scatter cursors start there.
-__global__ void k_bkt_bounds(const u32* col_off, u64 cols, u64 n, u32 nbkt, u32* rs, u32* cur) {
+__global__ void k_bkt_bounds(const u32* col_off, u64 cols, u64 n, u32 nbkt, u32 shift, u32* rs,
+                             u32* cur) {
     for (u64 b = blockIdx.x * (u64)blockDim.x + threadIdx.x; b <= nbkt;
          b += (u64)gridDim.x * blockDim.x) {
         u32 v = (u32)n;
         if (b < nbkt) {
-            const u64 target = b << kBktShift;
+            const u64 target = b << shift;
             u64 lo = 0, hi = cols + 1;  // col_off has cols + 1 entries, col_off[cols] = n
             while (lo < hi) {
                 const u64 m = (lo + hi) >> 1;
@@ -628,7 +630,8 @@ __global__ void k_bkt_bounds(const u32* col_off, u64 cols, u64 n, u32 nbkt, u32*
 
 __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 n, u32 bits_y,
                                                             const u32* col_off, u32* cur,
-                                                            u32 nbkt, u64* k_out, u32* v_out) {
+                                                            u32 nbkt, u32 shift, u64* k_out,
+                                                            u32* v_out) {
     extern __shared__ u32 sh_p1[];
     u32* hist = sh_p1;
     u32* base = sh_p1 + nbkt;
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 
             const u64 i = t0 + (u64)j * kP1Threads + threadIdx.x;
             br[j] = 0xffffffffu;
             if (i < n) {
-                const u32 b = __ldg(col_off + (k[j] >> bits_y)) >> kBktShift;
+                const u32 b = __ldg(col_off + (k[j] >> bits_y)) >> shift;
                 br[j] = (b << kP1RankBits) | atomicAdd(&hist[b], 1u);
             }
         }
@@ -671,15 +674,13 @@ __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 
 
 // Shared memory per P2 block: keys, perm, a per-slot u32 (column cursor /
 // column length, then union-find parent) and the slot's column start (u16).
-constexpr size_t kP2Smem = (size_t)kP2Cap * (8 + 4 + 4 + 2);
-
-template <bool kUnion>
-__global__ void __launch_bounds__(kP2Threads, 2) k_bkt_sort(const u64* kin, const u32* vin,
-                                                            const u32* rs, u32 nbkt,
-                                                            const u32* col_off, u32 bits_y,
-                                                            const u64* cnt_b, u64* skey,
-                                                            u32* perm, u32* parent, u32* size,
-                                                            u64* npts) {
+template <bool kUnion, int kP2Threads, int kMinBlocks>
+__global__ void __launch_bounds__(kP2Threads, kMinBlocks) k_bkt_sort(const u64* kin, const u32* vin,
+                                                                     const u32* rs, u32 nbkt,
+                                                                     const u32* col_off, u32 bits_y,
+                                                                     u64* skey, u32* perm,
+                                                                     u32* parent, u32* size) {
+    constexpr u32 kP2Cap = kP2Threads * kP2Items;
     extern __shared__ u64 sh_p2[];
     u64* sk = sh_p2;
     u32* sp = (u32*)(sk + kP2Cap);
@@ -1014,41 +1015,52 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     }
     const int gs = grid_for_s(n, L.n_sm, 16);
     int launches = cols && L.col_cnt ? 1 : 0;  // kernels launched (col_hist)
-    const u32 nbkt = (u32)((n + kBkt - 1) >> kBktShift);
+    const u64 mcol = L.host_ctr->max_col;
+    const u32 shift = mcol <= 1024 && ((n + 2047) >> 11) * 8 <= 96 * 1024 ? 11 : 12;
+    const u32 nbkt = (u32)((n + (1ull << shift) - 1) >> shift);
     const bool c1 = L.delta == 1 && !L.manhattan;
     bool bucket_counts = false;  // per-root counts already final (bucketed Chebyshev-1 path)
     static const int variant = [] {
         const char* v = std::getenv("RG_K3_SORT");
         return v && v[0] == 's' ? 1 : (v && v[0] == 'r' ? 2 : 0);
     }();
-    if (cols && L.col_cnt && variant == 0 && L.host_ctr->max_col <= kBktMaxCol &&
+    if (cols && L.col_cnt && variant == 0 && mcol <= kBktMaxCol &&
         (size_t)nbkt * 8 <= 96 * 1024) {  // L.flag holds >= 1024 and >= n entries
         // bucketed column sort (+ fused bucket-local unions for Chebyshev 1)
         e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
         if (e != cudaSuccess) return e;
         u32* rs = L.flag;  // nbkt + 1 region starts, then nbkt scatter cursors
         u32* cur = L.flag + nbkt + 1;
-        k_bkt_bounds<<<(nbkt + 256) / 256, 256, 0, st>>>(L.col_off, cols, n, nbkt, rs, cur);
+        k_bkt_bounds<<<(nbkt + 256) / 256, 256, 0, st>>>(L.col_off, cols, n, nbkt, shift, rs, cur);
         const size_t sm1 = (size_t)nbkt * 2 * sizeof(u32);
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_bkt_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  96 * 1024 + 1024);
-            cudaFuncSetAttribute(k_bkt_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kP2Smem);
-            cudaFuncSetAttribute(k_bkt_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kP2Smem);
+            cudaFuncSetAttribute(k_bkt_sort<true, 512, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(512));
+            cudaFuncSetAttribute(k_bkt_sort<false, 512, 2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(512));
+            cudaFuncSetAttribute(k_bkt_sort<true, 256, 4>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(256));
+            cudaFuncSetAttribute(k_bkt_sort<false, 256, 4>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(256));
             attr = true;
         }
         const u64 t1 = (n + kP1Tile - 1) / kP1Tile;
         const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * 4);
         k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, n, L.bits_y, L.col_off, cur, nbkt,
-                                                   L.ktmp, L.iota);
-        const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * 2);
+                                                   shift, L.ktmp, L.iota);
+        const bool small = shift == 11;
+        const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * (small ? 4 : 2));
+        auto p2 = [&](auto kernel, int threads) {
+            kernel<<<g2, threads, p2_smem(threads), st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
+                                                          L.bits_y, L.skey, L.perm, L.parent,
+                                                          L.size);
+        };
         if (c1) {
-            k_bkt_sort<true><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
-                                                              L.bits_y, L.sig_cnt, L.skey, L.perm,
-                                                              L.parent, L.size, L.npts);
+            if (small) p2(k_bkt_sort<true, 256, 4>, 256);
+            else p2(k_bkt_sort<true, 512, 2>, 512);
             launches += 5;  // scan (2), bounds, scatter, sort
             if (nbkt > 1) {
                 u32* linked = reinterpret_cast<u32*>(L.edges);  // >= 2n u32 entries
@@ -1063,9 +1075,8 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
             bucket_counts = true;
             if (L.npts_deferred) *L.npts_deferred = true;
         } else {
-            k_bkt_sort<false><<<g2, kP2Threads, kP2Smem, st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
-                                                               L.bits_y, L.sig_cnt, L.skey, L.perm,
-                                                               L.parent, L.size, L.npts);
+            if (small) p2(k_bkt_sort<false, 256, 4>, 256);
+            else p2(k_bkt_sort<false, 512, 2>, 512);
             launches += 5;
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

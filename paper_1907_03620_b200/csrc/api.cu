@@ -196,6 +196,9 @@ struct rg_ctx {
     u64 s_cols = 0;
     bool col_hist_ready = false;  // s_col_cnt holds the histogram of the current sig set (K2)
     bool npts_pending = false;    // sorted K3 left per-cluster point totals to rg_get_clusters
+    u32* slot_of = nullptr;       // sorted path: table slot of significant tile pos (K2)
+    bool sig_deferred = false;    // K2 left the table's SIG marks to mark_table()
+    bool table_cids = false;      // table count words hold SIG | (cluster id + 1)
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -420,6 +423,8 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
     ctx->ps_used = 0;
     ctx->used = 0;
     ctx->col_hist_ready = false;
+    ctx->sig_deferred = false;
+    ctx->table_cids = false;
     ctx->table_dirty = false;
     ctx->state = rg_ctx::kAccum;
     ctx->n_sig = 0;
@@ -734,6 +739,7 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     dfree(ctx->parent);
     dfree(ctx->size);
     dfree(ctx->tile_cid);
+    dfree(ctx->slot_of);
     dfree(ctx->root_cid);
     dfree(ctx->root_key);
     dfree(ctx->root_key_sorted);
@@ -750,6 +756,7 @@ rg_status ensure_sig_capacity(rg_ctx* ctx, u64 n) {
     CK(dalloc(&ctx->parent, c));
     CK(dalloc(&ctx->size, c));
     CK(dalloc(&ctx->tile_cid, c));
+    CK(dalloc(&ctx->slot_of, c));
     CK(dalloc(&ctx->root_cid, c));
     CK(dalloc(&ctx->root_key, c));
     CK(dalloc(&ctx->root_key_sorted, c));
@@ -785,6 +792,20 @@ rg_status ensure_col_arrays(rg_ctx* ctx, u64 cols) {
     CK(dalloc(&ctx->s_col_cnt, cols + 1));
     CK(dalloc(&ctx->s_col_off, cols + 1));
     ctx->s_cols = cols;
+    return RG_OK;
+}
+
+// The table's SIG marks after a sorted-path K2 (which records slot_of
+// instead of rewriting the table): SIG | (cluster id + 1) once clusters
+// exist (K4 then resolves a tile with one table load), else SIG | dense
+// index (the hash-probe K3's form).
+rg_status mark_table(rg_ctx* ctx, bool with_cids) {
+    if (!ctx->sig_deferred) return RG_OK;
+    CK(launch_mark_sig(table_of(ctx), ctx->slot_of, with_cids ? ctx->tile_cid : nullptr,
+                       ctx->n_sig, ctx->n_sm, ctx->st));
+    ++ctx->launches;
+    ctx->sig_deferred = false;
+    ctx->table_cids = with_cids;
     return RG_OK;
 }
 
@@ -828,10 +849,12 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
                           window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
                           ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
-                          ctx->root_cid, cols ? ctx->s_col_cnt : nullptr, ctx->ctr, ctx->n_sm,
-                          ctx->st));
+                          ctx->root_cid, cols ? ctx->s_col_cnt : nullptr,
+                          hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st));
         ++ctx->launches;
         ctx->col_hist_ready = cols != 0;
+        ctx->sig_deferred = !hash_k3;
+        ctx->table_cids = false;
     }
     return RG_OK;
 }
@@ -970,6 +993,10 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
         CK(cudaMemsetAsync(ctx->npts, 0, ctx->n_sig * sizeof(u64), ctx->st));
         CK(cudaMemsetAsync(ctx->min_key, 0xff, ctx->n_sig * sizeof(u64), ctx->st));
         CK(cudaMemsetAsync(ctx->root_cid, 0xff, ctx->n_sig * sizeof(int), ctx->st));
+    }
+    {
+        rg_status ms = mark_table(ctx, false);  // the hash-probe K3 resolves tiles via SIG marks
+        if (ms != RG_OK) return ms;
     }
     AggLaunch A;
     A.sig_key = ctx->sig_key;
@@ -1221,6 +1248,7 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->parent);
     dfree(ctx->size);
     dfree(ctx->tile_cid);
+    dfree(ctx->slot_of);
     dfree(ctx->root_cid);
     dfree(ctx->root_key);
     dfree(ctx->root_key_sorted);
@@ -1655,6 +1683,8 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     ctx->res = res;
     ctx->res_is_canvas = on_canvas;
     ctx->col_hist_ready = false;
+    ctx->sig_deferred = false;
+    ctx->table_cids = false;
     ctx->state = rg_ctx::kSig;
     ctx->sorted = false;
     ctx->table_dirty = true;
@@ -1924,9 +1954,13 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         }
         return RG_OK;
     }
+    {
+        rg_status ms = mark_table(ctx, true);
+        if (ms != RG_OK) return ms;
+    }
     if (kind == RG_MEM_DEVICE) {
-        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, labels, ctx->narrow,
-                               ctx->n_sm, ctx->st));
+        CK(launch_label_points(xy, n, ctx->grid, table_of(ctx), ctx->tile_cid, ctx->table_cids,
+                               labels, ctx->narrow, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaStreamSynchronize(ctx->st));
         return RG_OK;
@@ -1940,7 +1974,7 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
         CK(cudaMemcpyAsync(ctx->stage[b], xy + 2 * off, len * 16, cudaMemcpyHostToDevice,
                            ctx->st));
         CK(launch_label_points(ctx->stage[b], len, ctx->grid, table_of(ctx), ctx->tile_cid,
-                               ctx->lstage[b], ctx->narrow, ctx->n_sm, ctx->st));
+                               ctx->table_cids, ctx->lstage[b], ctx->narrow, ctx->n_sm, ctx->st));
         ++ctx->launches;
         CK(cudaMemcpyAsync(labels + off, ctx->lstage[b], len * 4, cudaMemcpyDeviceToHost,
                            ctx->st));
@@ -2002,8 +2036,12 @@ rg_status rg_cluster_points(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkin
         dxy = T.xy;
     }
     CK(dalloc(&T.lab, n));
-    CK(launch_label_points(dxy, n, ctx->grid, table_of(ctx), ctx->tile_cid, T.lab, ctx->narrow,
-                           ctx->n_sm, ctx->st));
+    {
+        rg_status ms = mark_table(ctx, true);
+        if (ms != RG_OK) return ms;
+    }
+    CK(launch_label_points(dxy, n, ctx->grid, table_of(ctx), ctx->tile_cid, ctx->table_cids, T.lab,
+                           ctx->narrow, ctx->n_sm, ctx->st));
     ++ctx->launches;
     CK(dalloc(&T.ia, n));
     CK(dalloc(&T.ib, n));

@@ -588,6 +588,7 @@ struct K2Out {
     int* root_cid;
     u32* col_cnt;  // sorted K3: per-column tile counts (key >> bits_y), or null
     u32 bits_y;
+    u32* slot_of;  // sorted K3: table slot of each significant tile (the table is not rewritten)
 };
 
 __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n, const K2Out& o,
@@ -609,7 +610,10 @@ __device__ __forceinline__ void k2_flush(const Table& t, const u32* s_idx, u32 n
             o.min_key[pos] = kEmpty;
             o.root_cid[pos] = -1;
         }
-        t.slots[i].count = kSigBit | pos;
+        if (o.slot_of)
+            o.slot_of[pos] = i;  // the table's SIG marks are written when K4 needs them
+        else
+            t.slots[i].count = kSigBit | pos;
     }
     if (o.col_cnt) {
         // column histogram of the sorted K3 (replaces its k_col_hist pass):
@@ -715,6 +719,24 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, cons
     if (slen) k2_flush(t, s_idx, slen, out, ctr, lane);
 }
 
+// Deferred SIG marks (sorted K3 path): the count word of significant tile
+// pos becomes SIG | pos (dense index, as K2 writes it on the hash path) or
+// SIG | (cluster id + 1) (K4's lookups then need no second load).
+__global__ void k_mark_sig(Table t, const u32* slot_of, const int* cid, u64 n) {
+    for (u64 pos = blockIdx.x * (u64)blockDim.x + threadIdx.x; pos < n;
+         pos += (u64)gridDim.x * blockDim.x)
+        t.slots[slot_of[pos]].count = kSigBit | (cid ? (u64)(u32)(cid[pos] + 1) : pos);
+}
+
+cudaError_t launch_mark_sig(Table t, const u32* slot_of, const int* cid, u64 n, int n_sm,
+                            cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const u64 want = (n + 255) / 256;
+    const int blocks = (int)(want < (u64)n_sm * 16 ? want : (u64)n_sm * 16);
+    k_mark_sig<<<blocks, 256, 0, st>>>(t, slot_of, cid, n);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 
 static int g_k1_warps_per_sm = 0;
@@ -791,7 +813,8 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
-                           u32* col_cnt, Counters* ctr, int n_sm, cudaStream_t st) {
+                           u32* col_cnt, u32* slot_of, Counters* ctr, int n_sm,
+                           cudaStream_t st) {
 #ifndef RG_K2_BPS
 #define RG_K2_BPS 16
 #endif
@@ -799,7 +822,8 @@ cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_k
     const u64 want = (cap + per_block - 1) / per_block;
     const u64 mx = (u64)n_sm * RG_K2_BPS;
     const int blocks = (int)(want < mx ? (want ? want : 1) : mx);
-    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid, col_cnt, t.bits_y};
+    const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid, col_cnt, t.bits_y,
+                  slot_of};
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, keep, o, ctr);
     return cudaGetLastError();
 }

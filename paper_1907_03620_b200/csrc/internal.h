@@ -37,7 +37,10 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
-                           u32* col_cnt, Counters* ctr, int n_sm, cudaStream_t st);
+                           u32* col_cnt, u32* slot_of, Counters* ctr, int n_sm,
+                           cudaStream_t st);
+cudaError_t launch_mark_sig(Table t, const u32* slot_of, const int* cid, u64 n, int n_sm,
+                            cudaStream_t st);
 cudaError_t launch_window_mark(Table t, u64 cap, u64 tau, u32 bits_x, u8* keep, int n_sm,
                                cudaStream_t st);
 
@@ -152,8 +155,11 @@ struct PointsLaunch {
 size_t cluster_points_temp_bytes(u64 m);
 cudaError_t launch_cluster_points(const PointsLaunch& L, cudaStream_t st);
 
+// table_cids: significant count words hold SIG | (cluster id + 1) (else SIG |
+// dense index into tile_cid)
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
-                                int* labels, bool narrow, int n_sm, cudaStream_t st);
+                                bool table_cids, int* labels, bool narrow, int n_sm,
+                                cudaStream_t st);
 
 // small utility kernels (api.cu)
 cudaError_t launch_iota(u32* out, u64 n, int n_sm, cudaStream_t st);

@@ -36,7 +36,7 @@ struct LSmem {
 // by position in an 8 x 16-tile window, as in K1); lanes that miss probe the
 // table themselves (equal keys in a row probe the same lines) and one lane
 // per slot installs the result.
-template <bool kNarrow>
+template <bool kNarrow, bool kCid>
 __device__ __forceinline__ int l_row(const Grid& g, const Table& t, const int* tile_cid, double x,
                                      double y, LSmem& w, int lane) {
     using K = KeyOps<kNarrow>;
@@ -49,7 +49,10 @@ __device__ __forceinline__ int l_row(const Grid& g, const Table& t, const int* t
     if (ballot(miss)) {
         if (miss) {
             const u64 v = table_find(t, K::table_key(key, g.bits_y));
-            cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
+            if (kCid)
+                cid = (v != kEmpty && (v & kSigBit)) ? (int)(u32)v - 1 : -1;
+            else
+                cid = (v != kEmpty && (v & kSigBit)) ? tile_cid[v & ~kSigBit] : -1;
             w.owner[cs] = (unsigned char)lane;
         }
         __syncwarp();
@@ -64,7 +67,7 @@ __device__ __forceinline__ int l_row(const Grid& g, const Table& t, const int* t
 
 // Segments of kLRowsPerSeg rows are dealt to warps round-robin; each warp
 // streams its rows through a per-lane cp.async ring like K1.
-template <bool kAligned, bool kNarrow>
+template <bool kAligned, bool kNarrow, bool kCid>
 __global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* xy, u64 n, Grid g,
                                                                   Table t, const int* tile_cid,
                                                                   int* labels) {
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* 
             for (int b = 0; b < kLBatch; ++b) issue(j + kLRing + b);
 #pragma unroll
             for (int b = 0; b < kLBatch; ++b) {
-                const int cid = l_row<kNarrow>(g, t, tile_cid, x[b], y[b], w, lane);
+                const int cid = l_row<kNarrow, kCid>(g, t, tile_cid, x[b], y[b], w, lane);
                 if ((j + b) * 32 + lane < valid) lab[(j + b) * 32] = cid;
             }
         }
@@ -132,11 +135,27 @@ __global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* 
 
 static int g_label_blocks_per_sm = 0;
 
+template <bool kCid>
+static void label_dispatch(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
+                           int* labels, bool narrow, int blocks, cudaStream_t st) {
+    const bool aligned = ((uintptr_t)xy & 15) == 0;
+    if (aligned && narrow)
+        k_label_points<true, true, kCid><<<blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+    else if (aligned)
+        k_label_points<true, false, kCid><<<blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+    else if (narrow)
+        k_label_points<false, true, kCid><<<blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+    else
+        k_label_points<false, false, kCid><<<blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+}
+
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
-                                int* labels, bool narrow, int n_sm, cudaStream_t st) {
+                                bool table_cids, int* labels, bool narrow, int n_sm,
+                                cudaStream_t st) {
     if (!g_label_blocks_per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_label_blocks_per_sm,
-                                                      k_label_points<true, false>, kLWarps * 32, 0);
+                                                      k_label_points<true, false, false>,
+                                                      kLWarps * 32, 0);
         if (g_label_blocks_per_sm < 1) g_label_blocks_per_sm = 1;
     }
     const u64 rows = (n + 31) / 32;
@@ -145,15 +164,10 @@ cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const 
     const u64 cap = (u64)n_sm * g_label_blocks_per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
-    const bool aligned = ((uintptr_t)xy & 15) == 0;
-    if (aligned && narrow)
-        k_label_points<true, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
-    else if (aligned)
-        k_label_points<true, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
-    else if (narrow)
-        k_label_points<false, true><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+    if (table_cids)
+        label_dispatch<true>(xy, n, g, t, tile_cid, labels, narrow, (int)blocks, st);
     else
-        k_label_points<false, false><<<(int)blocks, kLWarps * 32, 0, st>>>(xy, n, g, t, tile_cid, labels);
+        label_dispatch<false>(xy, n, g, t, tile_cid, labels, narrow, (int)blocks, st);
     return cudaGetLastError();
 }
 
