@@ -477,7 +477,7 @@ __global__ void k_sorted_label(const u32* parent, const u32* size, u64 mu, const
         const bool kept = size[r] >= mu;
         const int cid = kept ? (int)scan[r] : -1;
         cid_s[i] = cid;
-        tile_cid_b[perm[i]] = cid;
+        if (tile_cid_b) tile_cid_b[perm[i]] = cid;  // null: scattered on demand (api.cu)
         if (r == (u32)i) {
             ++roots;
             if (kept) clu_root[cid] = (u32)i;
@@ -591,10 +591,10 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
 // Every component's root is its smallest sorted index, as in the 256-tile
 // window kernels, so the reduce / id / label passes are shared.
 // ---------------------------------------------------------------------------
-// Bucket size 2^shift tiles (host-chosen, 11 or 12) and P2 block shapes:
-// 2048-tile buckets in 256-thread blocks (55 KB, 4 blocks per SM) when
-// every column holds <= 1024 tiles, else 4096-tile buckets in 512-thread
-// blocks (108 KB, 2 per SM) for columns of <= 2048 tiles.
+// Bucket size 2^shift tiles and P2 block shapes: 4096-tile buckets in
+// 512-thread blocks (108 KB, 2 per SM) for columns of <= 2048 tiles, or
+// (RG_BKT_SHIFT=11) 2048-tile buckets in 256-thread blocks (55 KB, 4 per
+// SM) when every column holds <= 1024 tiles.
 constexpr int kP1Threads = 512;
 constexpr int kP1Per = 16;              // keys per thread: 8192 per block
 constexpr u32 kP1Tile = kP1Threads * kP1Per;
@@ -1016,7 +1016,13 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     const int gs = grid_for_s(n, L.n_sm, 16);
     int launches = cols && L.col_cnt ? 1 : 0;  // kernels launched (col_hist)
     const u64 mcol = L.host_ctr->max_col;
-    const u32 shift = mcol <= 1024 && ((n + 2047) >> 11) * 8 <= 96 * 1024 ? 11 : 12;
+    // 4096-tile buckets by default; RG_BKT_SHIFT=11 selects 2048-tile buckets
+    // in 256-thread blocks (same P2 time, slower P1 on config 4)
+    static const bool small_bkt = [] {
+        const char* v = std::getenv("RG_BKT_SHIFT");
+        return v && std::atoi(v) == 11;
+    }();
+    const u32 shift = small_bkt && mcol <= 1024 && ((n + 2047) >> 11) * 8 <= 96 * 1024 ? 11 : 12;
     const u32 nbkt = (u32)((n + (1ull << shift) - 1) >> shift);
     const bool c1 = L.delta == 1 && !L.manhattan;
     bool bucket_counts = false;  // per-root counts already final (bucketed Chebyshev-1 path)

@@ -95,6 +95,29 @@ __global__ void k_gather_sorted(const u32* order, const u64* key, const u64* cnt
     }
 }
 
+// Cluster id per K2 index from the sorted ids (deferred by the sorted K3).
+__global__ void k_scatter_cid(const u32* perm, const int* cid_s, u64 n, int* tile_cid) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        tile_cid[perm[i]] = cid_s[i];
+}
+
+// Canonical output of the sorted path: keys and ids are already in sorted
+// order; only the counts are gathered through the permutation.
+__global__ void k_gather_sorted_keys(const u64* skey, const u32* perm, const u64* cnt,
+                                     const int* cid_s, u64 n, Grid res, long long* tx,
+                                     long long* ty, u64* cnt_out, long long* cid_out) {
+    const u64 ymask = (1ull << res.bits_y) - 1;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 k = skey[i];
+        if (tx) tx[i] = res.origin_x + (long long)(k >> res.bits_y);
+        if (ty) ty[i] = res.origin_y + (long long)(k & ymask);
+        if (cnt_out) cnt_out[i] = cnt[perm[i]];
+        if (cid_out) cid_out[i] = (long long)cid_s[i];
+    }
+}
+
 __global__ void k_cluster_facts(const u64* root_key_sorted, const u32* root_idx_sorted,
                                 const u32* clu_root, u64 n, const u32* size, const u64* npts,
                                 Grid res, u64* n_tiles, u64* n_points, long long* fx,
@@ -199,6 +222,7 @@ struct rg_ctx {
     u32* slot_of = nullptr;       // sorted path: table slot of significant tile pos (K2)
     bool sig_deferred = false;    // K2 left the table's SIG marks to mark_table()
     bool table_cids = false;      // table count words hold SIG | (cluster id + 1)
+    bool tile_cid_pending = false;  // sorted K3 left tile_cid (K2 order) to ensure_tile_cid()
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -425,6 +449,7 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
     ctx->col_hist_ready = false;
     ctx->sig_deferred = false;
     ctx->table_cids = false;
+    ctx->tile_cid_pending = false;
     ctx->table_dirty = false;
     ctx->state = rg_ctx::kAccum;
     ctx->n_sig = 0;
@@ -799,8 +824,26 @@ rg_status ensure_col_arrays(rg_ctx* ctx, u64 cols) {
 // instead of rewriting the table): SIG | (cluster id + 1) once clusters
 // exist (K4 then resolves a tile with one table load), else SIG | dense
 // index (the hash-probe K3's form).
+// Cluster id per K2 index (tile_cid), scattered from the sorted ids when the
+// device view, the labelling pass or the SIG marks need it.
+rg_status ensure_tile_cid(rg_ctx* ctx) {
+    if (!ctx->tile_cid_pending) return RG_OK;
+    if (ctx->n_sig) {
+        k_scatter_cid<<<grid_for(ctx->n_sig, ctx->n_sm), 256, 0, ctx->st>>>(
+            ctx->root_idx_sorted, ctx->s_cid, ctx->n_sig, ctx->tile_cid);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+    }
+    ctx->tile_cid_pending = false;
+    return RG_OK;
+}
+
 rg_status mark_table(rg_ctx* ctx, bool with_cids) {
     if (!ctx->sig_deferred) return RG_OK;
+    if (with_cids) {
+        rg_status s = ensure_tile_cid(ctx);
+        if (s != RG_OK) return s;
+    }
     CK(launch_mark_sig(table_of(ctx), ctx->slot_of, with_cids ? ctx->tile_cid : nullptr,
                        ctx->n_sig, ctx->n_sm, ctx->st));
     ++ctx->launches;
@@ -820,6 +863,7 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
     rg_status s = ensure_sig_capacity(ctx, ctx->used);
     if (s != RG_OK) return s;
     zero_field(ctx, &ctx->ctr->n_sig);
+    ctx->tile_cid_pending = false;
     if (ctx->slots && ctx->used) {
         const bool hash_k3 = !use_sorted_k3(ctx);
         if (window_fix) {
@@ -855,6 +899,7 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
         ctx->col_hist_ready = cols != 0;
         ctx->sig_deferred = !hash_k3;
         ctx->table_cids = false;
+    ctx->tile_cid_pending = false;
     }
     return RG_OK;
 }
@@ -938,7 +983,8 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     L.npts = ctx->npts;
     L.flag = ctx->s_flag;
     L.scan = ctx->s_scan;
-    L.tile_cid_b = ctx->tile_cid;
+    L.tile_cid_b = nullptr;  // K2-order ids are scattered on demand (ensure_tile_cid)
+    ctx->tile_cid_pending = true;
     L.cid_s = ctx->s_cid;
     L.clu_root = ctx->s_clu_root;
     L.edges = ctx->s_edges;
@@ -998,6 +1044,7 @@ rg_status agglomerate_impl(rg_ctx* ctx) {
         rg_status ms = mark_table(ctx, false);  // the hash-probe K3 resolves tiles via SIG marks
         if (ms != RG_OK) return ms;
     }
+    ctx->tile_cid_pending = false;  // the hash-probe K3 writes tile_cid itself
     AggLaunch A;
     A.sig_key = ctx->sig_key;
     A.sig_cnt = ctx->sig_cnt;
@@ -1685,6 +1732,7 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
     ctx->col_hist_ready = false;
     ctx->sig_deferred = false;
     ctx->table_cids = false;
+    ctx->tile_cid_pending = false;
     ctx->state = rg_ctx::kSig;
     ctx->sorted = false;
     ctx->table_dirty = true;
@@ -1842,9 +1890,16 @@ rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* co
         if (count) CK(salloc(&dcnt, w, ctx->st));
         if (cluster_id) CK(salloc(&dcid, w, ctx->st));
     }
-    CK(launch_gather_sorted(order, ctx->sig_key, ctx->sig_cnt,
-                            ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr, w, ctx->res,
-                            dtx, dty, dcnt, dcid, ctx->n_sm, ctx->st));
+    if (ctx->state == rg_ctx::kAgg && ctx->sorted) {
+        k_gather_sorted_keys<<<grid_for(w, ctx->n_sm), 256, 0, ctx->st>>>(
+            ctx->root_key_sorted, ctx->root_idx_sorted, ctx->sig_cnt, ctx->s_cid, w, ctx->res, dtx,
+            dty, dcnt, dcid);
+        CK(cudaGetLastError());
+    } else {
+        CK(launch_gather_sorted(order, ctx->sig_key, ctx->sig_cnt,
+                                ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr, w, ctx->res,
+                                dtx, dty, dcnt, dcid, ctx->n_sm, ctx->st));
+    }
     ++ctx->launches;
     if (kind == RG_MEM_HOST) {
         if (tx) CK(cudaMemcpyAsync(tx, dtx, w * 8, cudaMemcpyDeviceToHost, ctx->st));
@@ -1917,6 +1972,12 @@ rg_status rg_device_result(rg_ctx* ctx, rg_device_view* out) {
         return set_err(ctx, RG_ERR_STATE, "no significant tiles: call rg_prune first");
     out->key = (const uint64_t*)ctx->sig_key;
     out->count = (const uint64_t*)ctx->sig_cnt;
+    if (ctx->state == rg_ctx::kAgg) {
+        DevGuard guard(ctx->device);
+        rg_status s = ensure_tile_cid(ctx);
+        if (s != RG_OK) return s;
+        CK(cudaStreamSynchronize(ctx->st));
+    }
     out->cluster_id = ctx->state == rg_ctx::kAgg ? ctx->tile_cid : nullptr;
     out->n_significant = ctx->n_sig;
     out->n_clusters = ctx->n_kept;
@@ -1956,6 +2017,7 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
     }
     {
         rg_status ms = mark_table(ctx, true);
+        if (ms == RG_OK && !ctx->table_cids) ms = ensure_tile_cid(ctx);
         if (ms != RG_OK) return ms;
     }
     if (kind == RG_MEM_DEVICE) {
@@ -2038,6 +2100,7 @@ rg_status rg_cluster_points(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkin
     CK(dalloc(&T.lab, n));
     {
         rg_status ms = mark_table(ctx, true);
+        if (ms == RG_OK && !ctx->table_cids) ms = ensure_tile_cid(ctx);
         if (ms != RG_OK) return ms;
     }
     CK(launch_label_points(dxy, n, ctx->grid, table_of(ctx), ctx->tile_cid, ctx->table_cids, T.lab,

@@ -318,3 +318,22 @@ def test_cluster_facts_vs_oracle(k3):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("metric,delta,wf", [(Metric.chebyshev, 1, False), (Metric.chebyshev, 1, True),
+                                             (Metric.manhattan, 2, False), (Metric.chebyshev, 3, False)])
+def test_labels_every_k3_path_vs_oracle(metric, delta, wf):
+    """Per-point labels after the sorted K3 (table SIG marks written lazily,
+    carrying cluster ids) and after the hash-probe K3 (delta 3: SIG | dense
+    index written by K2); labelling twice gives the same answer."""
+    rng = np.random.default_rng(17 + delta)
+    gp = GridParams(precision=2, threshold=3, min_cluster_size=2, metric=metric, distance=delta)
+    c = rng.uniform([-170, -80], [170, 80], size=(300, 2))
+    pts = (c[rng.integers(0, 300, 200_000)] + rng.normal(0, 0.02, size=(200_000, 2))).astype(np.float64)
+    pl = Pipeline(gp)
+    pl.run(pts, use_window_fix=wf)
+    ref = O.port_cluster(pts, gp, window_fix=wf) if wf else O.port_cluster(pts, gp)
+    assert_same(pl.flat(), ref)
+    want = O.port_labels(pts, gp, ref)
+    assert np.array_equal(pl.label_points(pts), want)
+    assert np.array_equal(pl.label_points(pts), want)
