@@ -595,10 +595,17 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
 // 512-thread blocks (108 KB, 2 per SM) for columns of <= 2048 tiles, or
 // (RG_BKT_SHIFT=11) 2048-tile buckets in 256-thread blocks (55 KB, 4 per
 // SM) when every column holds <= 1024 tiles.
-constexpr int kP1Threads = 512;
-constexpr int kP1Per = 16;              // keys per thread: 8192 per block
+#ifndef RG_P1_THREADS
+#define RG_P1_THREADS 512
+#endif
+#ifndef RG_P1_PER
+#define RG_P1_PER 8
+#endif
+constexpr int kP1Threads = RG_P1_THREADS;
+constexpr int kP1Per = RG_P1_PER;       // keys per thread (512 x 8 = 4096 per block)
 constexpr u32 kP1Tile = kP1Threads * kP1Per;
 constexpr u32 kP1RankBits = 13;         // rank inside a block's tile < 8192
+static_assert(kP1Tile <= (1u << kP1RankBits), "P1 tile rank field");
 constexpr int kP2Items = 12;
 #ifndef RG_BKT_MAX_COL
 #define RG_BKT_MAX_COL 2048
@@ -1054,7 +1061,7 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
             attr = true;
         }
         const u64 t1 = (n + kP1Tile - 1) / kP1Tile;
-        const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * 4);
+        const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * (2048 / kP1Threads));
         k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, n, L.bits_y, L.col_off, cur, nbkt,
                                                    shift, L.ktmp, L.iota);
         const bool small = shift == 11;

@@ -173,6 +173,14 @@ struct rg_ctx {
     int n_sm = 148;
     int max_warps = 0;
     cudaStream_t own = nullptr, st = nullptr, copy_st = nullptr;
+    // Double-buffered table: the idle table is cleared on aux_st while the
+    // current step's K3 runs, so the next ingest starts on a clean table.
+    cudaStream_t aux_st = nullptr;
+    cudaEvent_t ev_alt = nullptr;  // recorded on aux_st after the idle table's clear
+    Slot* slots_alt = nullptr;
+    u64 cap_alt = 0;
+    bool alt_dirty = false;  // the idle table holds a previous step's entries
+    bool alt_ready = false;  // the idle table's clear is enqueued (ev_alt)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     cudaEvent_t ev_k2 = nullptr, ev_k3 = nullptr, ev_end = nullptr;  // fused prune + agglomerate
     cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
@@ -436,8 +444,35 @@ rg_status push_counters(rg_ctx* ctx) {
 rg_status reopen_accumulator(rg_ctx* ctx) {
     if (ctx->state == rg_ctx::kAccum && !ctx->table_dirty) return RG_OK;
     if (ctx->slots) {
-        CK(launch_table_clear(ctx->slots, ctx->cap, ctx->n_sm, ctx->st));
-        ++ctx->launches;
+        if (ctx->alt_ready && ctx->slots_alt && ctx->cap_alt == ctx->cap) {
+            // the idle table was cleared behind the previous step's K3
+            std::swap(ctx->slots, ctx->slots_alt);
+            CK(cudaStreamWaitEvent(ctx->st, ctx->ev_alt, 0));
+            ctx->alt_ready = false;
+            ctx->alt_dirty = true;
+        } else {
+            CK(launch_table_clear(ctx->slots, ctx->cap, ctx->n_sm, ctx->st));
+            ++ctx->launches;
+            if (ctx->slots_alt && ctx->cap_alt != ctx->cap) {
+                CK(cudaStreamSynchronize(ctx->aux_st));
+                dfree(ctx->slots_alt);
+                ctx->slots_alt = nullptr;
+                ctx->cap_alt = 0;
+                ctx->alt_ready = ctx->alt_dirty = false;
+            }
+            if (!ctx->slots_alt && ctx->cap * sizeof(Slot) <= (8ull << 30)) {
+                // second table (best effort: without it every step clears inline)
+                Slot* a = nullptr;
+                if (cudaMalloc(&a, ctx->cap * sizeof(Slot)) == cudaSuccess) {
+                    ctx->slots_alt = a;
+                    ctx->cap_alt = ctx->cap;
+                    ctx->alt_dirty = true;
+                    ctx->alt_ready = false;
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
     }
     if (ctx->ps && ctx->ps_used) {
         CK(cudaMemsetAsync(ctx->ps, 0xff, ctx->ps_cap * sizeof(PtKey), ctx->st));
@@ -897,6 +932,17 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
                           hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st));
         ++ctx->launches;
         ctx->col_hist_ready = cols != 0;
+        if (ctx->alt_dirty && ctx->slots_alt && ctx->cap_alt == ctx->cap) {
+            // clear the idle table on aux_st while K3 runs (K3 is not
+            // bandwidth-bound); the next ingest waits on ev_alt
+            CK(cudaEventRecord(ctx->ev_alt, ctx->st));
+            CK(cudaStreamWaitEvent(ctx->aux_st, ctx->ev_alt, 0));
+            CK(launch_table_clear(ctx->slots_alt, ctx->cap_alt, ctx->n_sm, ctx->aux_st));
+            ++ctx->launches;
+            CK(cudaEventRecord(ctx->ev_alt, ctx->aux_st));
+            ctx->alt_dirty = false;
+            ctx->alt_ready = true;
+        }
         ctx->sig_deferred = !hash_k3;
         ctx->table_cids = false;
     ctx->tile_cid_pending = false;
@@ -1240,6 +1286,10 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
     ctx->st = ctx->own;
     if ((e = cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(e, "stream");
+    if ((e = cudaStreamCreateWithFlags(&ctx->aux_st, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "stream");
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_alt, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(e, "event");
     if ((e = cudaEventCreate(&ctx->t0)) != cudaSuccess) return fail(e, "event");
     if ((e = cudaEventCreate(&ctx->ev_k2)) != cudaSuccess) return fail(e, "event");
     if ((e = cudaEventCreate(&ctx->ev_k3)) != cudaSuccess) return fail(e, "event");
@@ -1277,7 +1327,9 @@ void rg_destroy(rg_ctx* ctx) {
     DevGuard guard(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->copy_st) cudaStreamSynchronize(ctx->copy_st);
+    if (ctx->aux_st) cudaStreamSynchronize(ctx->aux_st);
     dfree(ctx->slots);
+    dfree(ctx->slots_alt);
     dfree(ctx->ctr);
     if (ctx->hctr) cudaFreeHost(ctx->hctr);
     dfree(ctx->part[0]);
@@ -1323,6 +1375,8 @@ void rg_destroy(rg_ctx* ctx) {
     if (ctx->ev_k3) cudaEventDestroy(ctx->ev_k3);
     if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
     if (ctx->t1) cudaEventDestroy(ctx->t1);
+    if (ctx->ev_alt) cudaEventDestroy(ctx->ev_alt);
+    if (ctx->aux_st) cudaStreamDestroy(ctx->aux_st);
     if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
