@@ -233,22 +233,24 @@ def ours(args) -> None:
         result_ctx = pl.ctx
         launches_of = pl.launches
     else:
-        # N>1: the union of all ranks' shards is clustered (exchange by tile
-        # owner, prune, all-gather of the significant set; distributed.py)
+        # N>1: the union of all ranks' shards is clustered: counts routed to
+        # the owner of their column range (NCCL all_to_all), each owner prunes
+        # and agglomerates its own columns, border join (distributed.py)
         from paper_1907_03620_b200.distributed import DistributedPipeline
 
         pl = DistributedPipeline(gp, device=local, stream=stream.cuda_stream)
-        result_ctx = pl.engine.agg
+        result_ctx = pl.engine.owner
         launches_of = pl.engine.launches
 
     def step_stats(ret):
         """(ms_contract, rg_stats-like facts) of the step just run."""
         if world == 1:
             return ret.ms_contract, ret
-        loc, agg = pl.engine.local.stats(), result_ctx.stats()
-        agg.ms_contract, agg.peak_accumulator_entries = loc.ms_contract, loc.peak_accumulator_entries
-        agg.ms_prune = pl.engine.owner.stats().ms_prune
-        return loc.ms_contract, agg
+        loc, own = pl.engine.local.stats(), result_ctx.stats()
+        own.ms_contract, own.peak_accumulator_entries = loc.ms_contract, loc.peak_accumulator_entries
+        own.n_significant = ret.n_significant
+        own.n_clusters = pl.stats_n_clusters
+        return loc.ms_contract, own
 
     def barrier():
         if dist:
@@ -283,22 +285,33 @@ def ours(args) -> None:
     # e2e: through the public API from pinned host memory, reading the
     # canonical result (sorted significant tiles + counts + cluster ids) back.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    S = st.n_significant
+    S = st.n_significant if world == 1 else int(pl.part[0].numel())  # this rank's columns
     # the result lands in pinned host buffers (as the input comes from one)
     pinned = [torch.empty(max(S, 1), dtype=torch.int64, pin_memory=True) for _ in range(4)]
     tx, ty, cnt, cid = (p.numpy() for p in pinned)
     from paper_1907_03620_b200 import _native as N
 
-    pl.run(host)  # untimed: first host-path call allocates the staging buffers
+    def readback():
+        if world == 1:
+            result_ctx.check(result_ctx.lib.rg_get_significant(
+                result_ctx.h, tx.ctypes.data, ty.ctypes.data, cnt.ctypes.data, cid.ctypes.data, S,
+                N.RG_MEM_HOST))
+        else:  # this rank's columns of the canonical result (global ids)
+            for dst, src in zip(pinned, pl.part):
+                dst[: src.numel()].copy_(src, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+    # untimed: the first host-path call allocates the staging buffers, the
+    # first readback the result buffers
+    pl.run(host)
+    readback()
     barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(e2e_steps):
         pl.run(host)
-        result_ctx.check(result_ctx.lib.rg_get_significant(
-            result_ctx.h, tx.ctypes.data, ty.ctypes.data, cnt.ctypes.data, cid.ctypes.data, S,
-            N.RG_MEM_HOST))
+        readback()
     f1.record(stream)
     barrier()
     ms_e2e = f0.elapsed_time(f1) / e2e_steps
@@ -341,8 +354,9 @@ def ours(args) -> None:
                    "l2": "inputs 8 GB >> 126 MB L2 each step (no flush needed)" if n >= 100_000_000
                    else "inputs smaller than L2: not flushed",
                    "parallelism": "1 GPU" if world == 1 else
-                   f"{world} ranks: own shard each, counts exchanged by tile owner "
-                   "(NCCL all_to_all), significant set all-gathered, K3 on every rank"},
+                   f"{world} ranks: own shard each, counts routed to the owner of their "
+                   "column range (NCCL all_to_all), K2+K3 per owner on its columns, "
+                   "border join of the range edges (small all_gathers)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": k1_traffic(n) if cfg == 4 else None,
                      "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01)",
@@ -379,7 +393,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--order", choices=["gen", "shuffled"], default="gen")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--ref-sample", type=int, default=20_000_000)
     ap.add_argument("--ref-workers", type=int, default=None)

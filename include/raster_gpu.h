@@ -216,6 +216,13 @@ rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
 rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                         uint32_t flags, rg_stats* stats);
 
+/* The prune + agglomerate half of cluster_sequential (pipeline.hpp:103-108)
+ * on what the context has accumulated so far (rg_ingest / rg_ingest_counts /
+ * rg_merge), with one host synchronisation: the owner step of a multi-rank
+ * run, whose counts arrive through rg_ingest_counts. flags as rg_cluster_ex;
+ * stats may be NULL. */
+rg_status rg_prune_agglomerate(rg_ctx* ctx, uint32_t flags, rg_stats* stats);
+
 /* RASTER' output (Mode::retain_points: take_points agglomerate.hpp:70-76 and
  * the point sort of finalize_clusters :183): every in-bounds point of xy
  * whose tile belongs to a kept cluster, grouped by cluster id and ordered by

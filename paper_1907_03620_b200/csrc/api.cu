@@ -1909,6 +1909,26 @@ rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind ki
     return RG_OK;
 }
 
+rg_status rg_prune_agglomerate(rg_ctx* ctx, uint32_t flags, rg_stats* stats) {
+    if (!ctx) return RG_ERR_ARG;
+    if (flags & ~(uint32_t)RG_CLUSTER_WINDOW_FIX)
+        return set_err(ctx, RG_ERR_ARG, "unknown rg_prune_agglomerate flags 0x%x", flags);
+    DevGuard guard(ctx->device);
+    rg_status s = RG_OK;
+    const u64 peak = ctx->used;
+    const bool wf = (flags & RG_CLUSTER_WINDOW_FIX) != 0;
+    if (ctx->state == rg_ctx::kAccum && use_sorted_k3(ctx)) {
+        s = prune_agglomerate_fused(ctx, wf);
+    } else {
+        s = prune_impl(ctx, wf);
+        if (s == RG_OK) s = agglomerate_impl(ctx);
+    }
+    if (s != RG_OK) return s;
+    ctx->used = peak;
+    if (stats) return rg_get_stats(ctx, stats);
+    return RG_OK;
+}
+
 rg_status rg_get_significant(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* count,
                              int64_t* cluster_id, uint64_t cap, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;

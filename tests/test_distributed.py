@@ -6,6 +6,7 @@ when both ranks' counts are added. The per-rank engine is a numpy double
 runs the same code in test_gpu_distributed.py."""
 from __future__ import annotations
 
+import dataclasses
 import os
 import socket
 
@@ -53,21 +54,25 @@ class NumpyEngine:
         return (torch.tensor(keys, dtype=torch.int64),
                 torch.tensor([c for _, c in items], dtype=torch.int64))
 
-    def owner_prune(self, keys, cnts):
+    def key_column(self, keys):
+        return keys >> 32
+
+    def column_x(self, col):
+        return int(col) - _OFF
+
+    def owner_cluster(self, keys, cnts):
         k, inv = np.unique(keys.numpy(), return_inverse=True)
         tot = np.bincount(inv, weights=cnts.numpy().astype(np.float64), minlength=k.size)
         keep = tot >= self.gp.threshold
         k, tot = k[keep], tot[keep].astype(np.int64)
         tx, ty = (k >> 32) - _OFF, (k & 0xFFFFFFFF) - _OFF
-        return torch.from_numpy(tx), torch.from_numpy(ty), torch.from_numpy(tot)
-
-    def agglomerate(self, tx, ty, cnt):
-        r = O.port_agglomerate(tx.numpy(), ty.numpy(), cnt.numpy().astype(np.uint64), self.gp)
-        self.res = FlatClustering(r.tx, r.ty, r.count, r.cluster_id, r.n_clusters, PipelineStats())
-        return len(r.tx), r.n_clusters
-
-    def flat(self):
-        return self.res
+        g1 = dataclasses.replace(self.gp, min_cluster_size=1)
+        r = O.port_agglomerate(tx, ty, tot.astype(np.uint64), g1)
+        size = np.bincount(r.cluster_id, minlength=r.n_clusters) if len(r.tx) else np.zeros(0)
+        return (torch.from_numpy(r.tx.astype(np.int64)), torch.from_numpy(r.ty.astype(np.int64)),
+                torch.from_numpy(r.count.astype(np.int64)),
+                torch.from_numpy(r.cluster_id.astype(np.int64)),
+                torch.from_numpy(size.astype(np.int64)))
 
 
 def _free_port() -> int:
@@ -142,3 +147,32 @@ def test_empty_rank(tmp_path):
     gp = GridParams(precision=1.0, threshold=2, min_cluster_size=1)
     pts = np.repeat(np.array([[0.05, 0.05], [0.15, 0.05]]), 3, axis=0)
     _check(_run([pts, np.zeros((0, 2))], gp, tmp_path), pts, gp)
+
+
+def test_components_across_ranks_three_ranks(tmp_path):
+    """Column-partitioned agglomeration: a chain spanning every rank's
+    columns, and dominoes placed so that every possible range boundary cuts
+    one of them in two — those reach mu = 2 only when joined across ranks
+    (P-RASTER's border join, parallel.hpp:146-352)."""
+    gp = GridParams(precision=0.0, threshold=1, distance=1, min_cluster_size=2)
+    tiles = [(x, 0) for x in range(-150, 150)]
+    for row, off in ((20, 0), (40, 1), (60, 2)):
+        for x in range(-150 + off, 148, 3):
+            tiles += [(x, row), (x + 1, row)]
+    tiles += [(-100, -50), (100, -50)]  # singletons: dropped by mu
+    pts = np.array(tiles, np.float64) + 0.5
+    rng = np.random.default_rng(2)
+    rng.shuffle(pts)
+    shards = [pts[0::3], pts[1::3], pts[2::3]]
+    _check(_run(shards, gp, tmp_path, world=3), pts, gp)
+
+
+def test_manhattan_delta2_across_ranks(tmp_path):
+    """Border strips are `distance` columns wide: Manhattan delta 2 joins
+    (x, y) with (x+2, y) and (x+1, y+1) across a range edge."""
+    gp = GridParams(precision=0.0, threshold=1, distance=2, metric=1, min_cluster_size=3)
+    rng = np.random.default_rng(9)
+    tiles = {(int(x), int(y)) for x, y in rng.integers([-120, -60], [120, 60], size=(2500, 2))}
+    pts = np.array(sorted(tiles), np.float64) + 0.5
+    rng.shuffle(pts)
+    _check(_run([pts[0::2], pts[1::2]], gp, tmp_path), pts, gp)

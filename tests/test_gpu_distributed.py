@@ -6,6 +6,7 @@ exchange, not a stand-in for multi-GPU timing. Needs a B200."""
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import os
 
 import numpy as np
@@ -35,13 +36,15 @@ def test_export_then_ingest_counts_roundtrip():
     k1, c1 = eng.export()
     k2, c2 = eng2.export()
     assert int(c1.sum() + c2.sum()) == eng.counters()[0] + eng2.counters()[0]
-    tx, ty, cnt = eng.owner_prune(torch.cat([k1, k2]), torch.cat([c1, c2]))
+    tx, ty, cnt, cid, size = eng.owner_cluster(torch.cat([k1, k2]), torch.cat([c1, c2]))
     ref = oracle(pts, gp)
     assert np.array_equal(tx.cpu().numpy(), ref.tx)
     assert np.array_equal(ty.cpu().numpy(), ref.ty)
     assert np.array_equal(cnt.cpu().numpy().astype(np.uint64), ref.count.astype(np.uint64))
-    assert eng.agglomerate(tx, ty, cnt) == (len(ref.tx), ref.n_clusters)
-    assert_same(eng.flat(), ref)
+    # the owner's components are found with mu = 1 (the filter is global)
+    ref1 = oracle(pts, dataclasses.replace(gp, min_cluster_size=1))
+    assert np.array_equal(cid.cpu().numpy(), ref1.cluster_id)
+    assert np.array_equal(size.cpu().numpy(), np.bincount(ref1.cluster_id))
 
 
 def test_export_host_and_ingest_counts_host():

@@ -29,3 +29,8 @@ print('torch h2d 8GB ms', t(lambda: dev.copy_(host, non_blocking=True)))
 ptx = torch.empty(S, dtype=torch.int64, pin_memory=True); pty = torch.empty(S, dtype=torch.int64, pin_memory=True)
 pcnt = torch.empty(S, dtype=torch.int64, pin_memory=True); pcid = torch.empty(S, dtype=torch.int64, pin_memory=True)
 print('get_significant pinned ms', t(lambda: pl.ctx.lib.rg_get_significant(pl.ctx.h, ptx.data_ptr(), pty.data_ptr(), pcnt.data_ptr(), pcid.data_ptr(), S, N.RG_MEM_HOST)))
+for k in range(3):
+    print('repeat', k, 'host run ms', t(lambda: pl.run(host), 1), 'torch h2d ms', t(lambda: dev.copy_(host, non_blocking=True), 1))
+import subprocess
+print(subprocess.run(['nvidia-smi', 'topo', '-m'], capture_output=True, text=True).stdout)
+print(subprocess.run(['bash', '-c', 'numactl -H 2>/dev/null | head -5; nproc; lscpu | grep -i "numa\\|model name"'], capture_output=True, text=True).stdout)
