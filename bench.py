@@ -341,6 +341,27 @@ def ours(args) -> None:
         extra["labelled"] = {"points_per_s": n / (ms_l / 1e3), "ms_per_step": ms_l,
                              "roofline_frac_20B": (20 * n / (ms_l / 1e3)) / (peak * 1e9)}
         del labels
+    if not args.quick and world == 1 and args.order == "gen":
+        # the same workload in a seeded random order (the reference generator
+        # shuffles, datagen.hpp:224-226): no spatial locality for K1's cache,
+        # every point reaches the HBM table
+        g = torch.Generator(device=dev.device)
+        g.manual_seed(11)
+        shuf = dev[torch.randperm(n, device=dev.device, generator=g)]
+        for _ in range(args.warmup):
+            pl.run(shuf)
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            pl.run(shuf)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ms_s = s0.elapsed_time(s1) / args.steps
+        extra["shuffled"] = {"points_per_s": n / (ms_s / 1e3), "ms_per_step": ms_s,
+                             "order": "torch.randperm(seed 11) on the device"}
+        del shuf
 
     peak, peak_src = measured_peak_gbs()
     k1_ms = statistics.mean(ms_contract)

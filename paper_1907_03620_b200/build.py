@@ -20,7 +20,7 @@ CSRC = PKG / "csrc"
 GPU_LIB = PKG / "libraster_b200.so"
 GEN_LIB = PKG / "libraster_datagen.so"
 
-CUDA_SOURCES = ["contract.cu", "agglomerate.cu", "agglomerate_sorted.cu", "label.cu", "points.cu", "dedupe.cu", "api.cu"]
+CUDA_SOURCES = ["contract.cu", "agglomerate.cu", "agglomerate_sorted.cu", "label.cu", "points.cu", "dedupe.cu", "partition.cu", "api.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -231,6 +231,16 @@ struct rg_ctx {
     bool sig_deferred = false;    // K2 left the table's SIG marks to mark_table()
     bool table_cids = false;      // table count words hold SIG | (cluster id + 1)
     bool tile_cid_pending = false;  // sorted K3 left tile_cid (K2 order) to ensure_tile_cid()
+    // contraction of unordered inputs (partition.cu)
+    void* part_scratch = nullptr;
+    size_t part_scratch_bytes = 0;
+    u64* pair_key = nullptr;
+    u32* pair_cnt = nullptr;
+    u64 pair_cap = 0;
+    u64 order_probe[2] = {0, 0};
+    const double* probe_ptr = nullptr;  // last probed buffer and its verdict
+    u64 probe_n = 0;
+    bool probe_unordered = false;
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -456,6 +466,9 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
             if (ctx->slots_alt && ctx->cap_alt != ctx->cap) {
                 CK(cudaStreamSynchronize(ctx->aux_st));
                 dfree(ctx->slots_alt);
+    if (ctx->part_scratch) cudaFree(ctx->part_scratch);
+    dfree(ctx->pair_key);
+    dfree(ctx->pair_cnt);
                 ctx->slots_alt = nullptr;
                 ctx->cap_alt = 0;
                 ctx->alt_ready = ctx->alt_dirty = false;
@@ -512,6 +525,80 @@ struct PhaseTimer {
 
 // K1 driver over a device-resident span (TileAccumulator::ingest
 // accumulator.hpp:120-134). Handles budget stops, growth and resumption.
+// Inputs without spatial order take the partitioned contraction
+// (partition.cu). RG_INGEST=k1 / =part forces a path; otherwise a probe of
+// 64 windows of 4096 consecutive points decides: when more than a quarter
+// of a window's points open a new tile, K1's per-warp cache cannot help.
+bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
+    static const int forced = [] {
+        const char* v = std::getenv("RG_INGEST");
+        return v ? (std::strcmp(v, "k1") == 0 ? 1 : (std::strcmp(v, "part") == 0 ? 2 : 0)) : 0;
+    }();
+    const u32 bits = ctx->grid.bits_x + ctx->grid.bits_y;
+    if (forced == 1 || !partition_ingest_supported(bits, n)) return false;
+    if (forced == 2) return true;
+    if (n < (1ull << 22)) return false;
+    // the same buffer clustered again (a serving loop, the bench) keeps its
+    // verdict: the probe's host round trip is paid once per buffer
+    if (ctx->probe_ptr == xy && ctx->probe_n == n) return ctx->probe_unordered;
+    if (launch_order_probe(xy, n, ctx->grid, ctx->scratch, ctx->n_sm, ctx->st) != cudaSuccess)
+        return false;
+    ++ctx->launches;
+    if (cudaMemcpyAsync(ctx->order_probe, ctx->scratch, 2 * sizeof(u64), cudaMemcpyDeviceToHost,
+                        ctx->st) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->st) != cudaSuccess)
+        return false;
+    const u64 distinct = ctx->order_probe[0], valid = ctx->order_probe[1];
+    ctx->probe_ptr = xy;
+    ctx->probe_n = n;
+    ctx->probe_unordered = valid > 0 && distinct * 5 > valid * 3;  // > 60 % open a new tile
+    return ctx->probe_unordered;
+}
+
+rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
+    size_t scan_temp = 0;
+    const size_t need = partition_scratch_bytes(n, &scan_temp);
+    if (ctx->part_scratch_bytes < need) {
+        if (ctx->part_scratch) cudaFree(ctx->part_scratch);
+        ctx->part_scratch = nullptr;
+        ctx->part_scratch_bytes = 0;
+        CK(cudaMalloc(&ctx->part_scratch, need));
+        ctx->part_scratch_bytes = need;
+    }
+    if (ctx->pair_cap < n) {  // one pair slot per point: per-unit slabs never overlap
+        dfree(ctx->pair_key);
+        dfree(ctx->pair_cnt);
+        ctx->pair_cap = 0;
+        CK(dalloc(&ctx->pair_key, n));
+        CK(dalloc(&ctx->pair_cnt, n));
+        ctx->pair_cap = n;
+    }
+    PartitionPlan plan;
+    PhaseTimer timer(ctx, &ctx->ms_contract);
+    PartitionLaunch L;
+    L.xy = xy;
+    L.n = n;
+    L.g = ctx->grid;
+    L.key_bits = ctx->grid.bits_x + ctx->grid.bits_y;
+    L.ctr = ctx->ctr;
+    L.scratch = ctx->part_scratch;
+    L.scan_temp = scan_temp;
+    L.pkey = ctx->pair_key;
+    L.pcnt = ctx->pair_cnt;
+    L.n_sm = ctx->n_sm;
+    CK(launch_partition_count(L, ctx->st, &plan));
+    ctx->launches += 5;  // hist, scan (2), scatter, aggregate
+    const u64 pairs = plan.pair_off.back();
+    // the table must hold every key KP3 can claim below the load target
+    while ((double)(ctx->used + pairs + plan.raw_points) >= kMaxLoad * (double)ctx->cap) {
+        rg_status s = grow_table(ctx, ctx->cap * 2);
+        if (s != RG_OK) return s;
+    }
+    CK(launch_partition_insert(L, table_of(ctx), plan, ctx->st));
+    ctx->launches += 1 + (plan.raw_points ? 1 : 0);
+    return pull_counters(ctx);
+}
+
 rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
     if (n == 0) return RG_OK;
     const u64 rows = (n + 31) / 32;
@@ -543,6 +630,8 @@ rg_status ingest_device(rg_ctx* ctx, const double* xy, u64 n) {
         rg_status s = grow_table(ctx, cap_min);
         if (s != RG_OK) return s;
     }
+
+    if (use_partition_ingest(ctx, xy, n)) return ingest_partitioned(ctx, xy, n);
 
     zero_field(ctx, &ctx->ctr->ticket);
     zero_field(ctx, &ctx->ctr->n_partial);

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace rg {
@@ -134,6 +136,35 @@ cudaError_t launch_ps_fold(const PtKey* src, u64 src_cap, Grid g, PointSet dst, 
 cudaError_t launch_ps_rehash(const PtKey* src, u64 src_cap, PointSet dst, int n_sm,
                              cudaStream_t st);
 cudaError_t launch_dedupe_counts(Table t, u64 cap, Table ut, int n_sm, cudaStream_t st);
+
+// contraction for unordered inputs (partition.cu)
+struct PartitionLaunch {
+    const double* xy;
+    u64 n;
+    Grid g;
+    u32 key_bits;
+    Counters* ctr;
+    void* scratch;      // partition_scratch_bytes(n)
+    size_t scan_temp;
+    u64* pkey;          // n entries: (key, count) pairs, one slab per work unit
+    u32* pcnt;
+    int n_sm;
+};
+bool partition_ingest_supported(u32 key_bits, u64 n);
+size_t partition_scratch_bytes(u64 n, size_t* scan_temp);
+cudaError_t launch_order_probe(const double* xy, u64 n, Grid g, u64* out, int n_sm,
+                               cudaStream_t st);
+struct PartitionPlan {
+    std::vector<uint4> units;   // (first, end, partition) of every KP2 work unit
+    std::vector<u32> dcnt;      // distinct tiles per unit (0xffffffff: overflowed)
+    std::vector<u64> pair_off;  // exclusive prefix of dcnt (overflowed units add 0)
+                                // (pairs live in per-unit slabs at units[u].x)
+    u64 raw_points = 0;         // points of overflowed units (added one by one)
+};
+cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, PartitionPlan* plan);
+cudaError_t launch_partition_insert(const PartitionLaunch& L, Table t, const PartitionPlan& plan,
+                                    cudaStream_t st);
+u32 partition_count();
 
 // RASTER' cluster points (points.cu)
 struct PointsLaunch {

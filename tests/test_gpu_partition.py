@@ -1,0 +1,94 @@
+"""The partitioned contraction (csrc/partition.cu) for inputs without
+spatial order: bit-exact against the CPU oracle, with the path forced
+(RG_INGEST=part) or chosen by the order probe, across chunked ingestion,
+out-of-bounds and NaN points, multi-round partitions and the per-point
+fallback for partitions that exceed every round. Each case runs in a fresh
+process because the switches are read once. Needs a B200."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+_SCRIPT = r"""
+import numpy as np, torch
+from oracle import pyoracle as O
+from paper_1907_03620_b200 import datagen as D
+from paper_1907_03620_b200.raster import GridParams, Pipeline, TileAccumulator
+from tests.gpu_util import assert_same
+case = {case!r}
+if case == "config2_shuffled":
+    gp = D.params(2)
+    pts = D.generate(D.spec(2, 0.5), shuffle_seed=7)
+    pts[::997] = [400.0, 0.0]
+    pts[5::1009] = [np.nan, 1.0]
+elif case == "config4_slice_shuffled":
+    gp = D.params(4)
+    pts = D.generate(D.spec(4, 0.02), shuffle_seed=8)  # 10M points
+elif case == "uniform_many_tiles":
+    gp = GridParams(precision=3, threshold=2, min_cluster_size=2)
+    rng = np.random.default_rng(4)
+    pts = np.concatenate([rng.uniform([-180, -90], [180, 90], size=(30_000_000, 2)),
+                          rng.normal([10, 10], 0.01, size=(2_000_000, 2))])
+    rng.shuffle(pts)
+else:
+    raise SystemExit("unknown case")
+dev = torch.from_numpy(pts).cuda()
+pl = Pipeline(gp)
+st = pl.run(dev)
+ref = O.port_cluster(pts, gp)
+assert_same(pl.flat(), ref)
+assert st.n_points == len(pts) and st.n_skipped == int(np.count_nonzero(
+    ~((pts[:, 0] >= gp.bounds.x_min) & (pts[:, 0] <= gp.bounds.x_max)
+      & (pts[:, 1] >= gp.bounds.y_min) & (pts[:, 1] <= gp.bounds.y_max))))
+# chunked, out of order: counts must not depend on the chunking
+acc = TileAccumulator(gp)
+n = len(pts)
+for a, b in ((n // 2, n), (0, n // 3), (n // 3, n // 2)):
+    acc.ingest(dev[a:b])
+tx, ty, cnt = acc.count_arrays()
+b = gp.bounds
+inb = (pts[:, 0] >= b.x_min) & (pts[:, 0] <= b.x_max) & (pts[:, 1] >= b.y_min) & (pts[:, 1] <= b.y_max)
+sc = 10.0 ** gp.precision
+q = pts[inb]
+kx = np.floor(q[:, 0] * sc).astype(np.int64) + (1 << 31)
+ky = np.floor(q[:, 1] * sc).astype(np.int64) + (1 << 31)
+uk, uc = np.unique((kx.astype(np.uint64) << np.uint64(32)) | ky.astype(np.uint64), return_counts=True)
+ak = ((tx + (1 << 31)).astype(np.uint64) << np.uint64(32)) | (ty + (1 << 31)).astype(np.uint64)
+o = np.argsort(ak)
+assert np.array_equal(ak[o], uk) and np.array_equal(cnt[o], uc.astype(np.uint64))
+assert acc.total_ingested() == int(inb.sum())
+print("ok")
+"""
+
+
+def _run(case: str, **env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", _SCRIPT.format(case=case)], cwd=str(ROOT), env=e,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("case", ["config2_shuffled", "config4_slice_shuffled"])
+def test_forced_partition_path(case):
+    _run(case, RG_INGEST="part")
+
+
+def test_auto_probe_picks_a_correct_path():
+    _run("config4_slice_shuffled")
+
+
+def test_multi_round_partitions():
+    """~32M distinct tiles: more than one shared-memory round per partition."""
+    _run("uniform_many_tiles", RG_INGEST="part")
+
+
+def test_per_point_fallback():
+    """One round allowed: partitions that overflow it take the per-point path."""
+    _run("uniform_many_tiles", RG_INGEST="part", RG_PART_MAX_ROUNDS="1")

@@ -8,7 +8,7 @@ build() {
     local name="$1"; shift
     (cd "$csrc" && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
         -Xcompiler -fPIC -Xcompiler -O3 -shared "$@" -o "$root/var/lib_$name.so" \
-        contract.cu agglomerate.cu agglomerate_sorted.cu label.cu points.cu dedupe.cu api.cu) &
+        contract.cu agglomerate.cu agglomerate_sorted.cu label.cu points.cu dedupe.cu partition.cu api.cu) &
 }
 rm -f "$root"/var/lib_*.so
 for spec in "$@"; do
