@@ -535,7 +535,8 @@ bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
         return v ? (std::strcmp(v, "k1") == 0 ? 1 : (std::strcmp(v, "part") == 0 ? 2 : 0)) : 0;
     }();
     const u32 bits = ctx->grid.bits_x + ctx->grid.bits_y;
-    if (forced == 1 || !partition_ingest_supported(bits, n)) return false;
+    // the partitioned kernels read points as 16-byte double2
+    if (forced == 1 || !partition_ingest_supported(bits, n) || ((uintptr_t)xy & 15)) return false;
     if (forced == 2) return true;
     if (n < (1ull << 22)) return false;
     // the same buffer clustered again (a serving loop, the bench) keeps its

@@ -37,9 +37,17 @@ elif case == "uniform_many_tiles":
     pts = np.concatenate([rng.uniform([-180, -90], [180, 90], size=(30_000_000, 2)),
                           rng.normal([10, 10], 0.01, size=(2_000_000, 2))])
     rng.shuffle(pts)
+elif case == "unaligned":
+    gp = D.params(3)
+    pts = D.generate(D.spec(3, 0.05), shuffle_seed=9)  # 5M points
 else:
     raise SystemExit("unknown case")
 dev = torch.from_numpy(pts).cuda()
+if case == "unaligned":  # 8-byte aligned view: the double2 kernels must not see it
+    buf = torch.zeros(pts.size + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = dev.reshape(-1)
+    dev = buf[1:].view(-1, 2)
+    assert dev.data_ptr() % 16 == 8
 pl = Pipeline(gp)
 st = pl.run(dev)
 ref = O.port_cluster(pts, gp)
@@ -75,7 +83,7 @@ def _run(case: str, **env):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("case", ["config2_shuffled", "config4_slice_shuffled"])
+@pytest.mark.parametrize("case", ["config2_shuffled", "config4_slice_shuffled", "unaligned"])
 def test_forced_partition_path(case):
     _run(case, RG_INGEST="part")
 
