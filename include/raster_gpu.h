@@ -165,6 +165,17 @@ rg_status rg_key_packing(rg_ctx* ctx, int64_t* origin_x, int64_t* origin_y, uint
 rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint64_t cap,
                             uint64_t* n_out, rg_memkind kind);
 
+/* Multi-rank routing of exported pairs (device pointers): pair i goes to
+ * part p = number of bin_splits[0 .. n_parts-2] <= bin, where
+ * bin = ((key >> key_bits_y) - col_min) * 4096 / col_width (the column
+ * histogram bins the ranks agreed on). out_keys / out_counts receive the
+ * pairs grouped by part (part order; order inside a part unspecified);
+ * part_counts[n_parts] (device) the pairs per part. n_parts <= 1024. */
+rg_status rg_route_pairs(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts, uint64_t n,
+                         int64_t col_min, uint64_t col_width, const uint32_t* bin_splits,
+                         uint32_t n_parts, uint64_t* out_keys, uint64_t* out_counts,
+                         uint64_t* part_counts);
+
 /* Adds (packed key, count) pairs produced by rg_export_entries of an
  * accumulator with equal params: the counts-add half of
  * TileAccumulator::merge (accumulator.hpp:137-154) for pairs that arrive

@@ -127,6 +127,7 @@ GPU_SYMBOLS = {
     "rg_cluster": (ST, [P, P, U64, ST, C.POINTER(rg_stats)]),
     "rg_cluster_ex": (ST, [P, P, U64, ST, C.c_uint32, C.POINTER(rg_stats)]),
     "rg_prune_agglomerate": (ST, [P, C.c_uint32, C.POINTER(rg_stats)]),
+    "rg_route_pairs": (ST, [P, P, P, U64, I64, U64, P, C.c_uint32, P, P, P]),
     "rg_get_significant": (ST, [P, P, P, P, P, U64, ST]),
     "rg_get_clusters": (ST, [P, P, P, P, P, U64, ST]),
     "rg_device_result": (ST, [P, C.POINTER(rg_device_view)]),

@@ -141,6 +141,65 @@ __global__ void k_count_of(Table t, u64 key, u64* out) {
     *out = (v == kEmpty) ? 0 : v;
 }
 
+// Multi-rank routing (rg_route_pairs): part of a pair from its column bin.
+__device__ __forceinline__ u32 route_part(u64 key, u32 bits_y, long long col_min, u64 width,
+                                          const u32* splits, u32 n_splits) {
+    const u64 bin = (((key >> bits_y) - (u64)col_min) * 4096ull) / width;
+    u32 lo = 0, hi = n_splits;  // number of splits <= bin
+    while (lo < hi) {
+        const u32 mid = (lo + hi) >> 1;
+        if (splits[mid] <= bin) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_route_count(const u64* keys, u64 n, u32 bits_y, long long col_min, u64 width,
+                              const u32* splits, u32 n_parts, u64* part_counts) {
+    __shared__ u32 cnt[1024];
+    for (u32 i = threadIdx.x; i < n_parts; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[route_part(keys[i], bits_y, col_min, width, splits, n_parts - 1)], 1u);
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < n_parts; i += blockDim.x)
+        if (cnt[i]) atomicAdd(part_counts + i, (u64)cnt[i]);
+}
+
+__global__ void k_route_offsets(const u64* part_counts, u32 n_parts, u64* cursor) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        u64 s = 0;
+        for (u32 i = 0; i < n_parts; ++i) {
+            cursor[i] = s;
+            s += part_counts[i];
+        }
+    }
+}
+
+__global__ void k_route_scatter(const u64* keys, const u64* counts, u64 n, u32 bits_y,
+                                long long col_min, u64 width, const u32* splits, u32 n_parts,
+                                u64* cursor, u64* out_keys, u64* out_counts) {
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const bool v = i < n;
+        const u64 k = v ? keys[i] : 0;
+        const u32 p = v ? route_part(k, bits_y, col_min, width, splits, n_parts - 1) : 0xffffffffu;
+        const u32 peers = __match_any_sync(kFull, p);
+        const int leader = __ffs(peers) - 1;
+        u64 base = 0;
+        if (v && lane == leader) base = atomicAdd(cursor + p, (u64)__popc(peers));
+        base = __shfl_sync(kFull, base, leader);
+        if (v) {
+            const u64 at = base + __popc(peers & ((1u << lane) - 1));
+            out_keys[at] = k;
+            out_counts[at] = counts[i];
+        }
+    }
+}
+
 int grid_for(u64 n, int n_sm, int per_sm = 8) {
     const u64 want = (n + 255) / 256;
     const u64 cap = (u64)n_sm * per_sm;
@@ -1651,6 +1710,40 @@ rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint6
         dfree(dk);
         dfree(dc);
     }
+    return RG_OK;
+}
+
+rg_status rg_route_pairs(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts, uint64_t n,
+                         int64_t col_min, uint64_t col_width, const uint32_t* bin_splits,
+                         uint32_t n_parts, uint64_t* out_keys, uint64_t* out_counts,
+                         uint64_t* part_counts) {
+    if (!ctx) return RG_ERR_ARG;
+    if (n_parts == 0 || n_parts > 1024 || col_width == 0)
+        return set_err(ctx, RG_ERR_ARG, "rg_route_pairs: 1..1024 parts and a positive width");
+    if (!part_counts || (n && (!keys || !counts || !out_keys || !out_counts)) ||
+        (n_parts > 1 && !bin_splits))
+        return set_err(ctx, RG_ERR_ARG, "null buffer");
+    DevGuard guard(ctx->device);
+    CK(cudaMemsetAsync(part_counts, 0, n_parts * sizeof(u64), ctx->st));
+    if (n) {
+        u64* cursor = nullptr;
+        CK(salloc(&cursor, n_parts, ctx->st));
+        const u32 by = ctx->grid.bits_y;
+        const int g = grid_for(n, ctx->n_sm, 8);
+        const u64* k = (const u64*)keys;
+        const u64* c = (const u64*)counts;
+        u64* pc = (u64*)part_counts;
+        k_route_count<<<g, 256, 0, ctx->st>>>(k, n, by, (long long)col_min, col_width, bin_splits,
+                                              n_parts, pc);
+        k_route_offsets<<<1, 32, 0, ctx->st>>>(pc, n_parts, cursor);
+        k_route_scatter<<<g, 256, 0, ctx->st>>>(k, c, n, by, (long long)col_min, col_width,
+                                                bin_splits, n_parts, cursor, (u64*)out_keys,
+                                                (u64*)out_counts);
+        ctx->launches += 3;
+        CK(cudaGetLastError());
+        sfree(cursor, ctx->st);
+    }
+    CK(cudaStreamSynchronize(ctx->st));
     return RG_OK;
 }
 

@@ -121,6 +121,22 @@ class GpuEngine:
                                             C.byref(got), N.RG_MEM_DEVICE))
         return keys, cnts
 
+    def route(self, keys, cnts, cmin: int, width: int, splits):
+        """Pairs grouped by owner on the device (rg_route_pairs): (keys,
+        counts, pairs per owner)."""
+        torch = self.torch
+        n, world = int(keys.numel()), len(splits) + 1
+        ok = torch.empty_like(keys)
+        oc = torch.empty_like(cnts)
+        pc = torch.empty(world, dtype=torch.int64, device=self.dev)
+        sp = torch.tensor(splits if splits else [0], dtype=torch.int32, device=self.dev)
+        c = self.local
+        c.check(c.lib.rg_route_pairs(c.h, keys.data_ptr() if n else None,
+                                     cnts.data_ptr() if n else None, n, int(cmin), int(width),
+                                     sp.data_ptr(), world, ok.data_ptr() if n else None,
+                                     oc.data_ptr() if n else None, pc.data_ptr()))
+        return ok, oc, pc.cpu().tolist()
+
     def key_column(self, keys):
         """Canvas column of packed keys (key = col << bits_y | row)."""
         return keys >> self.bits_y
@@ -284,12 +300,15 @@ class DistributedPipeline:
         col = eng.key_column(keys)
         cmin, width, sp = self._splits(col, wire)
         if world > 1:
-            bins = ((col - cmin) * N_BINS) // width
-            owner = torch.searchsorted(torch.tensor(sp, dtype=torch.int64, device=col.device),
-                                       bins, right=True)
-            order = torch.argsort(owner, stable=True)
-            keys, cnts = keys[order], cnts[order]
-            send_counts = torch.bincount(owner, minlength=world).cpu().tolist()
+            if hasattr(eng, "route"):  # device kernel (GpuEngine)
+                keys, cnts, send_counts = eng.route(keys, cnts, cmin, width, sp)
+            else:  # engine doubles in the tests
+                bins = ((col - cmin) * N_BINS) // width
+                owner = torch.searchsorted(torch.tensor(sp, dtype=torch.int64, device=col.device),
+                                           bins, right=True)
+                order = torch.argsort(owner, stable=True)
+                keys, cnts = keys[order], cnts[order]
+                send_counts = torch.bincount(owner, minlength=world).cpu().tolist()
             keys, _ = _all_to_all(dist, group, keys, send_counts, torch)
             cnts, _ = _all_to_all(dist, group, cnts, send_counts, torch)
             st.bytes_sent = 16 * st.n_local_entries

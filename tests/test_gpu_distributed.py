@@ -125,3 +125,28 @@ def test_two_ranks_gpu_engine_match_oracle(cfg, tmp_path):
         assert np.array_equal(o["count"], ref.count.astype(np.uint64))
         assert np.array_equal(o["cid"], ref.cluster_id)
         assert o["n"].tolist() == [ref.n_clusters, len(pts)]
+
+
+def test_route_pairs_matches_host_routing():
+    """rg_route_pairs groups exported pairs by the owner of their column bin,
+    exactly as the host formula the engine doubles use."""
+    pts = D.generate(D.spec(3, 0.05), shuffle_seed=3)
+    gp = D.params(3)
+    eng = GpuEngine(gp, 0)
+    eng.ingest(pts)
+    keys, cnts = eng.export()
+    col = eng.key_column(keys)
+    cmin, width = int(col.min()), int(col.max() - col.min() + 1)
+    splits = [700, 1500, 1501, 3000]
+    ok, oc, pc = eng.route(keys, cnts, cmin, width, splits)
+    bins = ((col - cmin) * 4096) // width
+    owner = torch.searchsorted(torch.tensor(splits, device=keys.device), bins, right=True)
+    assert pc == torch.bincount(owner, minlength=5).cpu().tolist()
+    at = 0
+    for p in range(5):
+        want = keys[owner == p]
+        got = ok[at: at + pc[p]]
+        assert torch.equal(torch.sort(got).values, torch.sort(want).values)
+        at += pc[p]
+    ref = dict(zip(keys.cpu().tolist(), cnts.cpu().tolist()))
+    assert all(ref[k] == c for k, c in zip(ok.cpu().tolist(), oc.cpu().tolist()))
