@@ -2363,6 +2363,71 @@ rg_status rg_cluster_points(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkin
     CK(launch_label_points(dxy, n, ctx->grid, table_of(ctx), ctx->tile_cid, ctx->table_cids, T.lab,
                            ctx->narrow, ctx->n_sm, ctx->st));
     ++ctx->launches;
+    if (((uintptr_t)dxy & 15) == 0) {
+        // v2: counting sort by cluster, then a shared-memory sort per cluster
+        struct Tmp2 {
+            u64 *cnt = nullptr, *off = nullptr;
+            double* grp = nullptr;
+            u32 *flag = nullptr, *pos = nullptr;
+            void* temp = nullptr;
+            ~Tmp2() {
+                dfree(cnt);
+                dfree(off);
+                dfree(grp);
+                dfree(flag);
+                dfree(pos);
+                if (temp) cudaFree(temp);
+            }
+        } V;
+        PointsV2 P2;
+        CK(dalloc(&V.cnt, C + 1));
+        CK(dalloc(&V.off, C + 1));
+        P2.temp_bytes = cluster_points_v2_temp_bytes(n, C);
+        CK(cudaMalloc(&V.temp, P2.temp_bytes));
+        P2.xy = dxy;
+        P2.labels = T.lab;
+        P2.n = n;
+        P2.n_clusters = C;
+        P2.dedupe = ctx->p.dedupe_points ? 1 : 0;
+        P2.cnt = V.cnt;
+        P2.off = V.off;
+        P2.scratch = ctx->scratch;
+        P2.temp = V.temp;
+        P2.n_sm = ctx->n_sm;
+        u64 m = 0, mx = 0;
+        CK(launch_cluster_points_v2_count(P2, ctx->st, &m, &mx));
+        ctx->launches += 4;
+        if (mx <= cluster_points_v2_cap()) {
+            CK(dalloc(&ctx->cp_xy, 2 * std::max<u64>(m, 1)));
+            if (P2.dedupe) {
+                CK(dalloc(&V.grp, 2 * std::max<u64>(m, 1)));
+                CK(dalloc(&V.flag, std::max<u64>(m, 1)));
+                CK(dalloc(&V.pos, std::max<u64>(m, 1)));
+                P2.grp = (double2*)V.grp;
+                P2.out = (double2*)ctx->cp_xy;
+            } else {
+                P2.grp = (double2*)ctx->cp_xy;  // grouped and sorted in place: the output
+                P2.out = nullptr;
+            }
+            P2.flag = V.flag;
+            P2.pos = V.pos;
+            P2.out_off = ctx->cp_off;
+            CK(launch_cluster_points_v2(P2, m, ctx->st));
+            ctx->launches += P2.dedupe ? 5 : 2;
+            if (!P2.dedupe)
+                CK(cudaMemcpyAsync(ctx->cp_off, V.off, (C + 1) * sizeof(u64),
+                                   cudaMemcpyDeviceToDevice, ctx->st));
+            CK(cudaMemcpyAsync(&ctx->hctr->pad0[1], ctx->cp_off + C, sizeof(u64),
+                               cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            ctx->cp_n = ctx->hctr->pad0[1];
+            ctx->cp_valid = true;
+            if (n_points) *n_points = ctx->cp_n;
+            if (n_clusters) *n_clusters = C;
+            return RG_OK;
+        }
+        // a cluster larger than one block's shared memory: the radix path below
+    }
     CK(dalloc(&T.ia, n));
     CK(dalloc(&T.ib, n));
     CK(dalloc(&T.ka, n + 1));

@@ -188,6 +188,30 @@ cudaError_t launch_cluster_points(const PointsLaunch& L, cudaStream_t st);
 
 // table_cids: significant count words hold SIG | (cluster id + 1) (else SIG |
 // dense index into tile_cid)
+struct PointsV2 {
+    const double* xy;     // 16-byte aligned
+    const int* labels;
+    u64 n;
+    u64 n_clusters;
+    int dedupe;
+    u64* cnt;             // C + 1 (counts, then scatter cursors)
+    u64* off;             // C + 1 (cluster starts; the offsets without dedupe)
+    double2* grp;         // M points grouped by cluster (the output without dedupe)
+    u32* flag;            // M (dedupe)
+    u32* pos;             // M (dedupe)
+    double2* out;         // M (dedupe output)
+    u64* out_off;         // C + 1 (dedupe offsets)
+    u64* scratch;         // one u64
+    void* temp;
+    size_t temp_bytes;
+    int n_sm;
+};
+size_t cluster_points_v2_temp_bytes(u64 n, u64 C);
+u32 cluster_points_v2_cap();
+cudaError_t launch_cluster_points_v2_count(const PointsV2& L, cudaStream_t st, u64* m_host,
+                                           u64* max_host);
+cudaError_t launch_cluster_points_v2(const PointsV2& L, u64 m, cudaStream_t st);
+
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
                                 bool table_cids, int* labels, bool narrow, int n_sm,
                                 cudaStream_t st);

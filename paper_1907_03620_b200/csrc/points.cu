@@ -164,4 +164,212 @@ cudaError_t launch_cluster_points(const PointsLaunch& L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// v2 (default): group by cluster with a counting sort, then sort each
+// cluster's points in shared memory. The labelled points of a cluster are
+// few (config 4: about 500), so the per-cluster sort replaces the three
+// 64-bit radix passes over all M points; clusters larger than kCpCap take
+// the v1 path above.
+//   hist     — points per cluster (runs of equal labels pre-summed per warp);
+//   scan     — cluster starts off[c];
+//   scatter  — points into their cluster's range (order inside arbitrary);
+//   sort     — one block per cluster: bitonic sort of (x, y) order keys in
+//              shared memory, written back in place (the signs of zeros
+//              travel with the point); with dedupe, a flag per point that
+//              differs from its predecessor;
+//   (dedupe) — scan of the flags, emit, per-cluster offsets.
+// ---------------------------------------------------------------------------
+constexpr u32 kCpCap = 4096;
+constexpr int kCpThreads = 256;
+constexpr size_t kCpSmem = kCpCap * (8 + 8 + 1);
+
+// Per-warp runs of equal labels: returns, for the run head, the run length
+// (0 for other lanes) and every lane's rank inside its run.
+__device__ __forceinline__ u32 label_runs(int lab, int lane, u32* rank) {
+    const int prev = __shfl_up_sync(kFull, lab, 1);
+    const bool head = lane == 0 || prev != lab;
+    const u32 heads = __ballot_sync(kFull, head);
+    const u32 le = heads & (0xffffffffu >> (31 - lane));
+    const int hl = 31 - __clz(le);  // this lane's run head
+    *rank = (u32)(lane - hl);
+    const u32 after = heads & ~(0xffffffffu >> (31 - lane));  // heads above this lane
+    const int next = after ? __ffs(after) - 1 : 32;
+    return head ? (u32)(next - lane) : 0u;
+}
+
+__global__ void k_cp_hist(const int* labels, u64 n, u64* cnt) {
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int lab = i < n ? labels[i] : -1;
+        u32 rank;
+        const u32 len = label_runs(lab, lane, &rank);
+        if (len && lab >= 0) atomicAdd(cnt + lab, (u64)len);
+    }
+}
+
+__global__ void k_cp_max(const u64* off, u64 C, u64* mx) {
+    u64 m = 0;
+    for (u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x; c < C;
+         c += (u64)gridDim.x * blockDim.x)
+        m = max(m, off[c + 1] - off[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(mx, m);
+}
+
+__global__ void k_cp_scatter(const double2* xy, const int* labels, u64 n, u64* cursor,
+                             double2* grp) {
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int lab = i < n ? labels[i] : -1;
+        u32 rank;
+        const u32 len = label_runs(lab, lane, &rank);
+        u64 base = 0;
+        if (len && lab >= 0) base = atomicAdd(cursor + lab, (u64)len);
+        const int hl = lane - (int)rank;
+        base = __shfl_sync(kFull, base, hl);
+        if (lab >= 0) grp[base + rank] = xy[i];
+    }
+}
+
+__device__ __forceinline__ double from_ord(u64 k, bool neg_zero) {
+    const u64 b = (k >> 63) ? (k & ~(1ull << 63)) : ~k;
+    const double d = __longlong_as_double((long long)b);
+    return neg_zero ? -0.0 : d;
+}
+
+// one block per cluster (persistent); flag (dedupe) may be null
+__global__ void __launch_bounds__(kCpThreads) k_cp_sort(double2* grp, const u64* off, u64 C,
+                                                        u32* flag) {
+    extern __shared__ u64 sh_cp[];  // kCpSmem bytes
+    u64* kx = sh_cp;
+    u64* ky = sh_cp + kCpCap;
+    unsigned char* zs = (unsigned char*)(ky + kCpCap);  // bit 0: x was -0.0, bit 1: y -0.0
+    for (u64 c = blockIdx.x; c < C; c += gridDim.x) {
+        const u64 lo = off[c];
+        const u32 len = (u32)(off[c + 1] - lo);
+        if (len > kCpCap) continue;  // the host sends such inputs down the v1 path
+        u32 P = 2;
+        while (P < len) P <<= 1;
+        for (u32 i = threadIdx.x; i < P; i += kCpThreads) {
+            if (i < len) {
+                const double2 v = grp[lo + i];
+                kx[i] = ord_key(v.x);
+                ky[i] = ord_key(v.y);
+                zs[i] = (unsigned char)((v.x == 0.0 && signbit(v.x) ? 1 : 0) |
+                                        (v.y == 0.0 && signbit(v.y) ? 2 : 0));
+            } else {
+                kx[i] = ky[i] = ~0ull;
+                zs[i] = 0;
+            }
+        }
+        __syncthreads();
+        // bitonic network; compare-exchange c of a stage pairs
+        // i = c + (c & ~(j - 1)) with i + j, so every thread works
+        for (u32 k = 2; k <= P; k <<= 1) {
+            for (u32 j = k >> 1; j > 0; j >>= 1) {
+                for (u32 c = threadIdx.x; c < P / 2; c += kCpThreads) {
+                    const u32 i = c + (c & ~(j - 1)), l = i + j;
+                    const bool asc = (i & k) == 0;
+                    const u64 ax = kx[i], ay = ky[i], bx = kx[l], by = ky[l];
+                    const bool a_gt = ax > bx || (ax == bx && ay > by);
+                    if (a_gt == asc && (ax != bx || ay != by)) {
+                        kx[i] = bx;
+                        ky[i] = by;
+                        kx[l] = ax;
+                        ky[l] = ay;
+                        const unsigned char t = zs[i];
+                        zs[i] = zs[l];
+                        zs[l] = t;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (u32 i = threadIdx.x; i < len; i += kCpThreads) {
+            grp[lo + i] = make_double2(from_ord(kx[i], zs[i] & 1), from_ord(ky[i], zs[i] & 2));
+            if (flag) flag[lo + i] = i == 0 || kx[i] != kx[i - 1] || ky[i] != ky[i - 1];
+        }
+        __syncthreads();
+    }
+}
+
+// dedupe: kept points compacted; cluster c starts at pos[off[c]]
+__global__ void k_cp_emit(const double2* grp, const u32* flag, const u32* pos, u64 m,
+                          const u64* off, u64 C, double2* out, u64* out_off) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m;
+         i += (u64)gridDim.x * blockDim.x)
+        if (flag[i]) out[pos[i]] = grp[i];
+    for (u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x; c <= C;
+         c += (u64)gridDim.x * blockDim.x)
+        out_off[c] = off[c] < m ? pos[off[c]] : (m ? pos[m - 1] + flag[m - 1] : 0);
+}
+
+size_t cluster_points_v2_temp_bytes(u64 n, u64 C) {
+    size_t a = 0, b = 0;
+    cub::DeviceScan::ExclusiveSum((void*)nullptr, a, (const u64*)nullptr, (u64*)nullptr,
+                                  (int)(C + 1));
+    cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const u32*)nullptr, (u32*)nullptr, (int)n);
+    return std::max(a, b);
+}
+
+// Phase 1 (host synchronises): counts, offsets, M and the largest cluster.
+cudaError_t launch_cluster_points_v2_count(const PointsV2& L, cudaStream_t st, u64* m_host,
+                                           u64* max_host) {
+    cudaError_t e;
+    const int gs = grid_of(L.n, L.n_sm);
+    if ((e = cudaMemsetAsync(L.cnt, 0, (L.n_clusters + 1) * sizeof(u64), st)) != cudaSuccess)
+        return e;
+    k_cp_hist<<<gs, 256, 0, st>>>(L.labels, L.n, L.cnt);
+    size_t tb = L.temp_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(L.temp, tb, L.cnt, L.off, (int)(L.n_clusters + 1),
+                                           st)) != cudaSuccess)
+        return e;
+    if ((e = cudaMemsetAsync(L.scratch, 0, sizeof(u64), st)) != cudaSuccess) return e;
+    k_cp_max<<<grid_of(L.n_clusters, L.n_sm), 256, 0, st>>>(L.off, L.n_clusters, L.scratch);
+    if ((e = cudaMemcpyAsync(m_host, L.off + L.n_clusters, sizeof(u64), cudaMemcpyDeviceToHost,
+                             st)) != cudaSuccess)
+        return e;
+    if ((e = cudaMemcpyAsync(max_host, L.scratch, sizeof(u64), cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+        return e;
+    return cudaStreamSynchronize(st);
+}
+
+u32 cluster_points_v2_cap() { return kCpCap; }
+
+// Phase 2: scatter, per-cluster sort, (dedupe) compaction. Without dedupe
+// the grouped array is the output (grp == out) and off the offsets.
+cudaError_t launch_cluster_points_v2(const PointsV2& L, u64 m, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(L.cnt, L.off, (L.n_clusters + 1) * sizeof(u64),
+                             cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return e;
+    const int gs = grid_of(L.n, L.n_sm);
+    k_cp_scatter<<<gs, 256, 0, st>>>(reinterpret_cast<const double2*>(L.xy), L.labels, L.n, L.cnt,
+                                     L.grp);
+    const int gc = (int)std::min<u64>(L.n_clusters, (u64)L.n_sm * 4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cp_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCpSmem);
+        attr = true;
+    }
+    if (gc)
+        k_cp_sort<<<gc, kCpThreads, kCpSmem, st>>>(L.grp, L.off, L.n_clusters,
+                                                   L.dedupe ? L.flag : nullptr);
+    if (L.dedupe && m) {
+        size_t tb = L.temp_bytes;
+        if ((e = cub::DeviceScan::ExclusiveSum(L.temp, tb, L.flag, L.pos, (int)m, st)) !=
+            cudaSuccess)
+            return e;
+        k_cp_emit<<<grid_of(std::max<u64>(m, L.n_clusters + 1), L.n_sm), 256, 0, st>>>(
+            L.grp, L.flag, L.pos, m, L.off, L.n_clusters, L.out, L.out_off);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace rg

@@ -110,3 +110,54 @@ def test_points_no_clusters_and_empty():
     assert xy.shape == (0, 2) and off.tolist() == [0, 0]
     xy, off = pl.cluster_points(pts)
     assert xy.tolist() == [[0.5, 0.5], [0.5, 0.5], [0.51, 0.5]] and off.tolist() == [0, 3]
+
+
+@pytest.mark.parametrize("dedupe", [False, True])
+def test_points_many_small_clusters_shared_memory_sort(dedupe):
+    """Clusters of a few hundred points (the per-cluster shared-memory sort,
+    not the radix fallback), with exact duplicates and signed zeros."""
+    rng = np.random.default_rng(23)
+    gp = GridParams(precision=2.0, threshold=3, min_cluster_size=2)
+    c = rng.uniform([-150, -70], [150, 70], size=(3000, 2))
+    pts = c[rng.integers(0, 3000, 600_000)] + rng.normal(0, 0.004, size=(600_000, 2))
+    pts = np.concatenate([pts, pts[:50_000], [[0.0, -0.0], [-0.0, 0.0], [0.005, 0.005]] * 4])
+    rng.shuffle(pts)
+    gp.dedupe_points = dedupe
+    gp.mode = Mode.retain_points if dedupe else Mode.count_only
+    import torch
+
+    pl = Pipeline(gp)
+    dev = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    pl.run(dev)
+    xy, off = pl.cluster_points(dev)
+    if dedupe:  # the reference's own Mode::retain_points + dedupe_points output
+        if O.ref() is None:
+            pytest.skip("oracle/_ref not built")
+        cid, px, py = O.ref_prime_points(pts, gp, dedupe=True)
+        assert np.array_equal(xy[:, 0], px) and np.array_equal(xy[:, 1], py)
+        assert np.array_equal(np.repeat(np.arange(len(off) - 1), np.diff(off).astype(np.int64)),
+                              cid)
+        assert len(off) - 1 > 2000  # many clusters: the shared-memory sort
+    else:
+        exy, eoff = expected_points(pts, gp)
+        assert np.array_equal(off, eoff)
+        assert np.array_equal(xy, exy)
+
+
+def test_points_unaligned_device_buffer():
+    """An 8-byte aligned point buffer takes the radix path (16-byte loads
+    elsewhere) with the same output."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    gp = GridParams(precision=2.0, threshold=3, min_cluster_size=2)
+    c = rng.uniform([-150, -70], [150, 70], size=(500, 2))
+    pts = c[rng.integers(0, 500, 100_000)] + rng.normal(0, 0.004, size=(100_000, 2))
+    buf = torch.zeros(pts.size + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(pts.reshape(-1)).cuda()
+    view = buf[1:].view(-1, 2)
+    pl = Pipeline(gp)
+    pl.run(view)
+    xy, off = pl.cluster_points(view)
+    exy, eoff = expected_points(pts, gp)
+    assert np.array_equal(off, eoff) and np.array_equal(xy, exy)
