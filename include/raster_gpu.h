@@ -127,7 +127,9 @@ void rg_destroy(rg_ctx* ctx);
 const char* rg_last_error(const rg_ctx* ctx);
 
 /* Run the context's work on a caller stream (cudaStream_t as void*), e.g.
- * torch.cuda.current_stream().cuda_stream. NULL restores the private one. */
+ * torch.cuda.current_stream().cuda_stream. NULL restores the private one;
+ * pass cudaStreamLegacy ((void*)1) for the legacy default stream (handle 0
+ * would mean "private"). */
 rg_status rg_set_stream(rg_ctx* ctx, void* stream);
 rg_status rg_synchronize(rg_ctx* ctx);
 

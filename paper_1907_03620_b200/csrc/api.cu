@@ -297,6 +297,7 @@ struct rg_ctx {
     u32* pair_cnt = nullptr;
     u64 pair_cap = 0;
     u64 order_probe[2] = {0, 0};
+    int chunk_verdict = -1;  // host-span ingest: the first chunk's verdict for the rest
     const double* probe_ptr = nullptr;  // last probed buffer and its verdict
     u64 probe_n = 0;
     bool probe_unordered = false;
@@ -598,6 +599,7 @@ bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
     if (forced == 1 || !partition_ingest_supported(bits, n) || ((uintptr_t)xy & 15)) return false;
     if (forced == 2) return true;
     if (n < (1ull << 22)) return false;
+    if (ctx->chunk_verdict >= 0) return ctx->chunk_verdict != 0;
     // the same buffer clustered again (a serving loop, the bench) keeps its
     // verdict: the probe's host round trip is paid once per buffer
     if (ctx->probe_ptr == xy && ctx->probe_n == n) return ctx->probe_unordered;
@@ -612,6 +614,10 @@ bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
     ctx->probe_ptr = xy;
     ctx->probe_n = n;
     ctx->probe_unordered = valid > 0 && distinct * 5 > valid * 3;  // > 60 % open a new tile
+    if (g_debug)
+        std::fprintf(stderr, "[rg] order probe n=%llu: %llu of %llu sampled points open a tile -> %s\n",
+                     (unsigned long long)n, (unsigned long long)distinct,
+                     (unsigned long long)valid, ctx->probe_unordered ? "partitioned" : "K1");
     return ctx->probe_unordered;
 }
 
@@ -918,6 +924,14 @@ rg_status ingest_any(rg_ctx* ctx, const double* xy, u64 n, rg_memkind kind) {
         s = enqueue_copy(i);
         if (s != RG_OK) return s;
     }
+    // the order probe runs on the first chunk only; later chunks reuse its
+    // verdict (the staging buffers alternate, so the per-buffer memo would
+    // probe every chunk)
+    struct VerdictScope {
+        rg_ctx* c;
+        ~VerdictScope() { c->chunk_verdict = -1; }
+    } verdict_scope{ctx};
+    ctx->chunk_verdict = -1;
     for (u64 i = 0; i < chunks; ++i) {
         const int b = (int)(i & 1);
         const u64 off = i * ch;
@@ -925,6 +939,7 @@ rg_status ingest_any(rg_ctx* ctx, const double* xy, u64 n, rg_memkind kind) {
         CK(cudaStreamWaitEvent(ctx->st, ctx->copied[b], 0));
         s = ingest_span(ctx, ctx->stage[b], len, &oob, &ox, &oy);
         if (s != RG_OK) return s;
+        if (i == 0 && ctx->probe_ptr == ctx->stage[b]) ctx->chunk_verdict = ctx->probe_unordered;
         CK(cudaEventRecord(ctx->done[b], ctx->st));
         if (oob) {
             CK(cudaStreamSynchronize(ctx->copy_st));

@@ -48,7 +48,7 @@ import numpy as np
 
 from . import _native as N
 from .raster import (FlatClustering, GridParams, PipelineStats, _Context, _Points,
-                     neighbor_offsets)
+                     neighbor_offsets, stream_arg)
 
 N_BINS = 4096  # column histogram resolution for the range split
 
@@ -89,7 +89,7 @@ class GpuEngine:
         self.local = _Context(params, device)
         self.owner = _Context(dataclasses.replace(params, min_cluster_size=1), device)
         for c in (self.local, self.owner):
-            c.check(c.lib.rg_set_stream(c.h, stream))
+            c.check(c.lib.rg_set_stream(c.h, stream_arg(stream)))
         ox, oy, by = C.c_int64(), C.c_int64(), C.c_uint32()
         self.local.check(self.local.lib.rg_key_packing(self.local.h, C.byref(ox), C.byref(oy),
                                                        C.byref(by)))

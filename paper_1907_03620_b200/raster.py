@@ -177,6 +177,15 @@ class PipelineStats:
 
 
 # ---------------------------------------------------------- buffer helpers
+def stream_arg(stream_ptr: int | None):
+    """rg_set_stream argument for a cudaStream_t handle: None = the
+    context's private stream; 0 (the legacy default stream, which is what
+    torch.cuda.current_stream() reports by default) = cudaStreamLegacy."""
+    if stream_ptr is None:
+        return None
+    return 1 if int(stream_ptr) == 0 else int(stream_ptr)
+
+
 class _Points:
     """(pointer, n, memkind) view of a point buffer, keeping it alive."""
 
@@ -494,7 +503,11 @@ class Pipeline:
         self.ctx = _Context(params, device)
 
     def set_stream(self, stream_ptr: int | None) -> None:
-        self.ctx.check(self.ctx.lib.rg_set_stream(self.ctx.h, stream_ptr))
+        """Run on a caller stream, e.g. torch.cuda.current_stream().cuda_stream
+        (handle 0, torch's legacy default stream, is passed as
+        cudaStreamLegacy so the work stays ordered with it); None restores
+        the context's private stream."""
+        self.ctx.check(self.ctx.lib.rg_set_stream(self.ctx.h, stream_arg(stream_ptr)))
 
     def run(self, pts, use_window_fix: bool = False) -> N.rg_stats:
         """cluster_sequential pipeline.hpp:92-126 on the device; results stay
