@@ -310,3 +310,25 @@ def test_top_row_key_wrap_is_not_adjacency(monkeypatch, k3):
                          check=True).stdout.split("\n")[0]
     # (b,0)-(b+1,0) adjacent; (b,3) alone; (b+2,3) alone; (b+3,0) alone
     assert out == "4 [0, 1, 0, 2, 3]", out
+
+
+def test_stream_ordering_with_torch_default_stream():
+    """Points produced by a torch kernel on the default stream and clustered
+    right away (no synchronize) on that stream: set_stream(0) must order
+    the work after it (0 is torch's legacy default stream, passed as
+    cudaStreamLegacy), so the result equals that of settled data."""
+    torch = torch_mod()
+    pts = D.generate(D.spec(3, 0.3), shuffle_seed=2)  # 30M points, 480 MB
+    src = torch.from_numpy(pts).cuda()
+    torch.cuda.synchronize()
+    gp = D.params(3)
+    ref = Pipeline(gp)
+    ref.run(src)
+    want = ref.flat()
+    pl = Pipeline(gp)
+    pl.set_stream(torch.cuda.current_stream().cuda_stream)
+    for _ in range(3):
+        dst = torch.empty_like(src)
+        dst.copy_(src.flip(0))  # still running when the next call is enqueued
+        pl.run(dst)
+        assert_same(pl.flat(), want)
