@@ -439,6 +439,8 @@ Grid make_grid(const rg_params& p) {
     g.y_max = p.y_max;
     g.origin_x = (long long)std::floor(p.x_min * g.scale);  // min_column core.hpp:117-119
     g.origin_y = (long long)std::floor(p.y_min * g.scale);
+    g.ox32 = (int)g.origin_x;
+    g.oy32 = (int)g.origin_y;
     const double cols = std::floor(p.x_max * g.scale) - std::floor(p.x_min * g.scale) + 1.0;
     const double rows = std::floor(p.y_max * g.scale) - std::floor(p.y_min * g.scale) + 1.0;
     g.bits_x = bits_for(cols);
@@ -1928,6 +1930,8 @@ rg_status rg_load_significant(rg_ctx* ctx, const int64_t* tx, const int64_t* ty,
                            "tile set spans too large a range for a 63-bit packed key");
         res.origin_x = mnx;
         res.origin_y = mny;
+        res.ox32 = (int)mnx;
+        res.oy32 = (int)mny;
         res.bits_x = bx;
         res.bits_y = by;
     }

@@ -66,6 +66,8 @@ struct Grid {
     long long origin_x, origin_y;
     u32 bits_y;
     u32 bits_x;
+    int ox32, oy32;  // origin_x / origin_y truncated (narrow canvases): a plain
+                     // 32-bit constant operand in the projection, no reload
 };
 
 #ifndef RG_BLOCK_BITS
@@ -236,8 +238,8 @@ struct KeyOps<true> {
     __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
         const int tx = __double2int_rd(__dmul_rn(x, g.scale));
         const int ty = __double2int_rd(__dmul_rn(y, g.scale));
-        const u32 kx = (u32)(tx - (int)g.origin_x);
-        const u32 ky = (u32)(ty - (int)g.origin_y);
+        const u32 kx = (u32)(tx - g.ox32);
+        const u32 ky = (u32)(ty - g.oy32);
         return in_bounds(g, x, y) ? (((u64)kx << 32) | ky) : kEmpty;
     }
     // Direct-mapped by position in an 8 x 16-tile window (low 3 column bits,

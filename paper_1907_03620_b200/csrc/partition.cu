@@ -165,7 +165,7 @@ __device__ __forceinline__ void block_scan_parts(const u32* in, u32* out, u32* w
 constexpr int kP1Thr = 1024;
 constexpr u32 kP1SubN = kP1Thr * kPSub;  // points per pass step
 constexpr u32 kSubN = 2 * kP1SubN;
-constexpr size_t kScatterSmem = (4 * kParts + kSubN + kP1Thr / 32) * 4 + kSubN * 2;
+constexpr size_t kScatterSmem = (5 * kParts + kSubN + kP1Thr / 32) * 4 + kSubN * 2;
 static_assert(kParts % kP1Thr == 0 && kParts % kPThreads == 0, "partition scan layout");
 
 // KP1: every in-bounds point's residual, written at its partition's place.
@@ -177,12 +177,16 @@ __global__ void __launch_bounds__(kP1Thr, 1) k_part_scatter(const double2* xy, u
     u32* hist = cur + kParts;       // this round's points per partition
     u32* loff = hist + kParts;      // exclusive prefix of hist
     u32* lcur = loff + kParts;      // placement cursors
-    u32* stage = lcur + kParts;
+    u32* pend = lcur + kParts;      // end of each partition's global range
+    u32* stage = pend + kParts;
     u32* wsum = stage + kSubN;
     unsigned short* spart = (unsigned short*)(wsum + kP1Thr / 32);
     const u64 pol = evict_first_policy();
     for (u64 t = blockIdx.x; t < T; t += gridDim.x) {
-        for (u32 p = threadIdx.x; p < kParts; p += kP1Thr) cur[p] = off_pt[p * T + t];
+        for (u32 p = threadIdx.x; p < kParts; p += kP1Thr) {
+            cur[p] = off_pt[p * T + t];
+            pend[p] = off_pt[(p + 1) * T];  // (p + 1) * T = kParts * T: the total
+        }
         const u64 p0 = t * kPTile, p1 = min(n, p0 + kPTile);
         for (u64 q0 = p0; q0 < p1; q0 += kSubN) {
             const u64 q1 = min(p1, q0 + kSubN);
@@ -231,7 +235,10 @@ __global__ void __launch_bounds__(kP1Thr, 1) k_part_scatter(const double2* xy, u
             const u32 cnt = loff[kParts - 1] + hist[kParts - 1];
             for (u32 i = threadIdx.x; i < cnt; i += kP1Thr) {
                 const u32 part = spart[i];
-                res[cur[part] + (i - loff[part])] = stage[i];
+                const u32 at = cur[part] + (i - loff[part]);
+                // KP0 counted exactly these points; the guard only matters if
+                // the buffer changed between the two passes (a caller race)
+                if (at < pend[part]) res[at] = stage[i];
             }
             __syncthreads();
             for (u32 p = threadIdx.x; p < kParts; p += kP1Thr) cur[p] += hist[p];
@@ -249,7 +256,11 @@ __device__ __forceinline__ void agg_insert(u32* skey, u32* scnt, u32* occ, u32* 
                                            u32 c) {
     const u32 k = r + 1;
     u32 s = (r * 0x9E3779B1u) >> (32 - 14);
-    while (true) {
+    for (u32 probes = 0;; ++probes) {
+        if (probes == kAggSlots) {  // full table: the unit is redone in more rounds
+            *over = 1;
+            return;
+        }
         const u32 cur = skey[s];
         if (cur == k) {
             atomicAdd(&scnt[s], c);

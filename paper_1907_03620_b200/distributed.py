@@ -88,6 +88,7 @@ class GpuEngine:
         self.dev = torch.device("cuda", device)
         self.local = _Context(params, device)
         self.owner = _Context(dataclasses.replace(params, min_cluster_size=1), device)
+        self.stream = stream
         for c in (self.local, self.owner):
             c.check(c.lib.rg_set_stream(c.h, stream_arg(stream)))
         ox, oy, by = C.c_int64(), C.c_int64(), C.c_uint32()
@@ -101,7 +102,7 @@ class GpuEngine:
 
     # -- step 1
     def ingest(self, pts) -> None:
-        p = _Points(pts)
+        p = _Points(pts, self.stream is None)
         self.local.check(self.local.lib.rg_ingest(self.local.h, p.ptr, p.n, p.kind))
 
     def counters(self):

@@ -189,7 +189,10 @@ def stream_arg(stream_ptr: int | None):
 class _Points:
     """(pointer, n, memkind) view of a point buffer, keeping it alive."""
 
-    def __init__(self, pts):
+    def __init__(self, pts, settle: bool = True):
+        """settle: a CUDA tensor may still be being written by torch's
+        current stream; unless the context runs on that stream
+        (set_stream), wait for it first."""
         self.keep = pts
         if hasattr(pts, "data_ptr") and hasattr(pts, "is_cuda"):
             import torch
@@ -201,6 +204,8 @@ class _Points:
             self.n = pts.shape[0] if pts.numel() else 0
             self.ptr = pts.data_ptr() if self.n else None
             self.kind = N.RG_MEM_DEVICE if pts.is_cuda else N.RG_MEM_HOST
+            if settle and pts.is_cuda and self.n:
+                torch.cuda.current_stream(pts.device).synchronize()
             return
         arr = np.asarray(pts, dtype=np.float64)
         if arr.size == 0:
@@ -331,7 +336,7 @@ class TileAccumulator:
 
     def ingest(self, pts) -> None:
         """accumulator.hpp:117-134 — any chunking, any order."""
-        p = _Points(pts)
+        p = _Points(pts, getattr(self, "_settle", True))
         self._ctx.check(self._ctx.lib.rg_ingest(self._ctx.h, p.ptr, p.n, p.kind))
 
     def merge(self, other: "TileAccumulator") -> None:
@@ -508,11 +513,12 @@ class Pipeline:
         cudaStreamLegacy so the work stays ordered with it); None restores
         the context's private stream."""
         self.ctx.check(self.ctx.lib.rg_set_stream(self.ctx.h, stream_arg(stream_ptr)))
+        self._settle = stream_ptr is None
 
     def run(self, pts, use_window_fix: bool = False) -> N.rg_stats:
         """cluster_sequential pipeline.hpp:92-126 on the device; results stay
         resident (device_view / flat / labels)."""
-        p = _Points(pts)
+        p = _Points(pts, getattr(self, "_settle", True))
         s = N.rg_stats()
         flags = N.RG_CLUSTER_WINDOW_FIX if use_window_fix else 0
         self.ctx.check(self.ctx.lib.rg_cluster_ex(self.ctx.h, p.ptr, p.n, p.kind, flags,
@@ -530,7 +536,7 @@ class Pipeline:
     def label_points(self, pts, out=None):
         """Per-point cluster ids (point-retaining variant). For device points
         `out` may be a preallocated int32 CUDA tensor."""
-        p = _Points(pts)
+        p = _Points(pts, getattr(self, "_settle", True))
         if p.kind == N.RG_MEM_DEVICE:
             import torch
             if out is None:
@@ -547,7 +553,7 @@ class Pipeline:
         """RASTER' output on the device (take_points agglomerate.hpp:70-76,
         finalize_clusters :183): (points (M, 2) float64 grouped by cluster id
         and point_less-sorted within a cluster, offsets (C + 1,) uint64)."""
-        p = _Points(pts)
+        p = _Points(pts, getattr(self, "_settle", True))
         m, c = C.c_uint64(), C.c_uint64()
         self.ctx.check(self.ctx.lib.rg_cluster_points(self.ctx.h, p.ptr, p.n, p.kind,
                                                       C.byref(m), C.byref(c)))
