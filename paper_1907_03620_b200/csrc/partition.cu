@@ -33,9 +33,9 @@
 // A partition is the low 11 bits of a bijective mix of the packed key
 // (multiply by an odd constant mod 2^B, then xor-shift by ceil(B/2)); the
 // other B-11 bits are the residual, so the key is recovered exactly. A unit
-// whose tiles do not fit 64 rounds of 12 Ki (not reachable below ~25G
-// distinct tiles) is flagged by KP2 and its points are added one by one by
-// KP3.
+// holds at most 256 Ki points, so 32 rounds of 12 Ki tiles always suffice;
+// the per-point fallback (a unit KP2 flags as overflowed, whose points KP3
+// adds one by one) is exercised with RG_PART_MAX_ROUNDS=1 in the tests.
 #include <cstdlib>
 #include <vector>
 
