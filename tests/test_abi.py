@@ -89,3 +89,14 @@ def test_no_device_means_error_not_fallback():
     assert st == N.RG_ERR_CUDA
     assert h.value is None
     assert lib.rg_last_error(None)
+
+
+def test_stream_handle_mapping():
+    """torch's legacy default stream reports handle 0, which the C-ABI reads
+    as "the context's private stream"; the Python layer passes it as
+    cudaStreamLegacy so work stays ordered with torch's producers."""
+    from paper_1907_03620_b200.raster import stream_arg
+
+    assert stream_arg(None) is None
+    assert stream_arg(0) == 1
+    assert stream_arg(0x7F00DEADBEEF) == 0x7F00DEADBEEF
