@@ -528,9 +528,6 @@ rg_status reopen_accumulator(rg_ctx* ctx) {
             if (ctx->slots_alt && ctx->cap_alt != ctx->cap) {
                 CK(cudaStreamSynchronize(ctx->aux_st));
                 dfree(ctx->slots_alt);
-    if (ctx->part_scratch) cudaFree(ctx->part_scratch);
-    dfree(ctx->pair_key);
-    dfree(ctx->pair_cnt);
                 ctx->slots_alt = nullptr;
                 ctx->cap_alt = 0;
                 ctx->alt_ready = ctx->alt_dirty = false;
@@ -1528,6 +1525,10 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->s_edges);
     dfree(ctx->s_col_cnt);
     dfree(ctx->s_col_off);
+    if (ctx->part_scratch) cudaFree(ctx->part_scratch);
+    ctx->part_scratch = nullptr;
+    dfree(ctx->pair_key);
+    dfree(ctx->pair_cnt);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {

@@ -237,10 +237,15 @@ def test_config5_scaled_vs_oracle():
 
 
 @pytest.mark.parametrize("cfg", [4, 5])
-def test_config_full_size_properties(cfg):
-    """Full BASELINE sizes (500M / 200M points): bit-identical results across
-    input order (generation vs shuffled) and across chunked ingestion;
-    label histogram consistent with per-cluster point counts."""
+def test_config_full_size_vs_oracle_and_properties(cfg):
+    """Full BASELINE sizes (500M / 200M points) against the CPU oracle
+    (the C restatement of cluster_sequential, pipeline.hpp:92-126, and of
+    labeled_points, metrics.hpp:78-83): significant tiles, counts, canonical
+    ids and counters bit-exact; config 4 also per point (int32 labels).
+    Then the same bytes in a seeded random order (config 4 takes the
+    partitioned contraction K1' there) and in 7 out-of-order chunks must give
+    bit-identical results, and the shuffled labels must be the permuted
+    generation-order labels."""
     torch = torch_cuda()
     s = D.spec(cfg)
     n = D.count(s)
@@ -251,16 +256,24 @@ def test_config_full_size_properties(cfg):
     pl = Pipeline(gp)
     st = pl.run(dev)
     a = pl.flat()
+    ref = oracle(host, gp)
+    assert_same(a, ref, f"cfg{cfg} full size vs oracle")
+    assert (st.n_ingested, st.n_skipped, st.peak_accumulator_entries) == (
+        ref.n_ingested, ref.n_skipped, ref.n_distinct)
     assert st.n_ingested + st.n_skipped == n
-    assert a.n_clusters > 0
-    # labels: count per cluster == sum of its tile counts
     labels = pl.label_points(dev)
-    hist = torch.bincount(labels[labels >= 0].long(), minlength=a.n_clusters).cpu().numpy()
-    keep = a.cluster_id >= 0
-    want = np.bincount(a.cluster_id[keep], weights=a.count[keep].astype(np.float64),
-                       minlength=a.n_clusters)
-    assert np.array_equal(hist.astype(np.float64), want)
-    del labels
+    if cfg == 4:
+        want_labels = O.port_labels(host, gp, ref)
+        assert np.array_equal(labels.cpu().numpy(), want_labels), "cfg4 per-point labels"
+        del want_labels
+    else:
+        # labels: count per cluster == sum of its tile counts
+        hist = torch.bincount(labels[labels >= 0].long(), minlength=a.n_clusters).cpu().numpy()
+        keep = a.cluster_id >= 0
+        want = np.bincount(a.cluster_id[keep], weights=a.count[keep].astype(np.float64),
+                           minlength=a.n_clusters)
+        assert np.array_equal(hist.astype(np.float64), want)
+    del ref, host
     # chunked ingestion (7 uneven chunks, out of order) == single pass
     acc = TileAccumulator(gp)
     cuts = sorted({0, n, *[int(v) for v in np.random.default_rng(3).integers(0, n, 6)]})
@@ -270,14 +283,37 @@ def test_config_full_size_properties(cfg):
     sig = acc.prune()
     assert np.array_equal(sig.tx, a.tx) and np.array_equal(sig.ty, a.ty)
     assert np.array_equal(sig.count, a.count)
+    del acc, sig
     # shuffled order (device-side permutation) == generation order
     perm = torch.randperm(n, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
     shuf = dev[perm]
-    del perm
     pl2 = Pipeline(gp)
     pl2.run(shuf)
-    b = pl2.flat()
-    assert_same(b, a, f"cfg{cfg} order invariance")
+    assert_same(pl2.flat(), a, f"cfg{cfg} order invariance")
+    assert torch.equal(pl2.label_points(shuf), labels[perm]), f"cfg{cfg} shuffled labels"
+
+
+def test_context_reuse_across_growth_and_partitioned_ingest():
+    """One Pipeline (one C-ABI context) reused: a shuffled run, a larger run
+    whose table grows, then a shuffled run of >= 4 Mi points (the partitioned
+    contraction's scratch must survive the table resize), each against the
+    oracle."""
+    torch = torch_cuda()
+    gp = D.params(3)
+    pl = Pipeline(gp)
+    noise = np.random.default_rng(12).uniform([-180, -90], [180, 90], size=(8_000_000, 2))
+    cases = (
+        ("shuffled 5M", D.generate(D.spec(3, 0.05), shuffle_seed=7)),
+        ("10M + 8M distinct noise tiles (table grows)",
+         np.concatenate([D.generate(D.spec(3, 0.1)), noise])),
+        ("shuffled 6M after the resize", D.generate(D.spec(3, 0.06), shuffle_seed=9)),
+    )
+    caps = []
+    for what, pts in cases:
+        st = pl.run(torch.from_numpy(pts).cuda())
+        caps.append(st.table_capacity)
+        assert_same(pl.flat(), oracle(pts, gp), what)
+    assert caps[1] > caps[0], caps  # the second step really grew the table
 
 
 @pytest.mark.parametrize("k3", ["bucket", "seg", "hash"])
