@@ -124,15 +124,29 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+def host_cpu() -> dict:
+    """nproc and the lscpu model name of this host."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count() or 1, "model": model}
+
+
 def reference_arm(args) -> None:
     """The reference's own CPU implementation (oracle/_ref = the reference
-    compiled from its headers) on this host's cores, on a bounded sample of
-    the same workload."""
+    compiled from its headers, raster::cluster_parallel with every host
+    thread) on the SAME workload as our arm (the full config by default).
+    When K full-size runs would not fit --ref-budget-s, fewer are timed and
+    the line says so (steps, steps_requested)."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import pyoracle as O
     from paper_1907_03620_b200 import datagen as D
 
@@ -143,52 +157,116 @@ def reference_arm(args) -> None:
     workers = args.ref_workers if args.ref_workers is not None else cores
     s = D.spec(args.config)
     per = s.points_per_cluster
-    sample_pts = min(args.ref_sample, D.count(s))
     full = D.count(s)
-    # bounded sample = the first clusters of the workload (generation order)
-    s.n_clusters = max(1, sample_pts // max(per, 1)) if per else s.n_clusters
+    if args.ref_sample and args.ref_sample < full:
+        # bounded sample = the first clusters of the workload (generation order)
+        s.n_clusters = max(1, args.ref_sample // max(per, 1)) if per else s.n_clusters
     pts = D.generate(s, shuffle_seed=(11 if args.order == "shuffled" else None))
-    gp = D.params(args.config)
-    times = []
-    for i in range(args.warmup + args.steps):
-        t, tp, tc, nc = O.ref_time(pts.ctypes.data, pts.shape[0], gp, workers)
-        if i >= args.warmup:
-            times.append(t)
     n = pts.shape[0]
+    gp = D.params(args.config)
+    t_start = time.perf_counter()
+    warm = []
+    for _ in range(max(1, args.warmup)):
+        warm.append(O.ref_time(pts.ctypes.data, n, gp, workers)[0])
+        if time.perf_counter() - t_start > args.ref_budget_s / 4:
+            break
+    per_run = min(warm)
+    steps = max(1, min(args.steps, int(args.ref_budget_s // max(per_run, 1e-9))))
+    times = [O.ref_time(pts.ctypes.data, n, gp, workers)[0] for _ in range(steps)]
     med = statistics.median(times)
     value = n / med
-    kind = "reference"
-    sample = (f"first {n:,} points ({s.n_clusters:,} clusters) of {WORKLOADS[args.config].split(':')[0]} "
-              f"({full:,} points), {args.order} order; raster::cluster_"
-              f"{'parallel' if workers else 'sequential'} count mode")
+    what = (f"all {n:,} points" if n == full else f"first {n:,} points ({s.n_clusters:,} clusters)")
+    sample = (f"{what} of {WORKLOADS[args.config].split(':')[0]} ({full:,} points), {args.order} order; "
+              f"raster::cluster_{'parallel' if workers else 'sequential'} count mode; median of "
+              f"{steps} timed runs after {len(warm)} warm-up")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": steps, "steps_requested": args.steps, "warmup": len(warm),
         "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "order": args.order,
+        "config": {"workload": WORKLOADS[args.config], "order": args.order, "points": n,
+                   "same_config": n == full,
                    "parallelism": f"cpu x{max(workers, 1)} threads"},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": max(workers, 1),
-                         "kind": kind, "sample": sample},
+                         "kind": "reference", "sample": sample, "host": host_cpu(),
+                         "runs_s": times},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def cpu_baseline_sequential(pts_host, gp, n_sample: int) -> dict:
-    """Reference cluster_sequential (1 core) on a bounded sample."""
+def cpu_baseline_sequential(pts_host, gp, n_count: int, n_retain: int) -> dict:
+    """The reference's cluster_sequential on 1 core: count mode over
+    n_count points (the whole workload by default, one run) and
+    Mode::retain_points (the point-retaining variant) over the first
+    n_retain points."""
     from oracle import pyoracle as O
 
     if O.ref() is None:
         t0 = time.perf_counter()
-        O.port_cluster(pts_host[:n_sample], gp)
+        O.port_cluster(pts_host[:n_count], gp)
         t = time.perf_counter() - t0
-        kind = "port"
-    else:
-        t, _, _, _ = O.ref_time(pts_host.ctypes.data, n_sample, gp, 0)
-        kind = "reference"
-    return {"value": n_sample / t, "unit": "points/s", "cores": 1, "kind": kind,
-            "sample": f"first {n_sample:,} points of the workload (generation order), "
-                      f"raster::cluster_sequential count mode, 1 thread"}
+        return {"value": n_count / t, "unit": "points/s", "cores": 1, "kind": "port",
+                "sample": f"first {n_count:,} points, oracle port, 1 thread", "host": host_cpu()}
+    t, tp, tc, _ = O.ref_time(pts_host.ctypes.data, n_count, gp, 0)
+    out = {"value": n_count / t, "unit": "points/s", "cores": 1, "kind": "reference",
+           "sample": (f"{'all' if n_count == len(pts_host) else 'first'} {n_count:,} points of the "
+                      "workload (generation order), raster::cluster_sequential count mode, "
+                      "1 thread, 1 run"),
+           "same_config": n_count == len(pts_host),
+           "phases_s": {"projection": tp, "clustering": tc}, "host": host_cpu()}
+    if n_retain:
+        tr, _, _, _ = O.ref_time_mode(pts_host.ctypes.data, n_retain, gp, 0, True)
+        out["retain_points"] = {
+            "value": n_retain / tr, "unit": "points/s", "cores": 1,
+            "sample": f"first {n_retain:,} points, raster::cluster_sequential Mode::retain_points, "
+                      "1 thread, 1 run (the reference's point-retaining variant)"}
+    return out
+
+
+def per_config_sweep(args, pl4, stream, dev4) -> dict:
+    """Every BASELINE config (1-5), in generation order and in a seeded random
+    order (device permutation): device time per rg_cluster call with the
+    points resident, points/s and the fraction of the 16 B/pt roofline."""
+    import torch
+
+    from paper_1907_03620_b200 import datagen as D
+    from paper_1907_03620_b200.raster import Pipeline
+
+    peak, _ = measured_peak_gbs()
+    out = {}
+    for cfg in (1, 2, 3, 4, 5):
+        if cfg == 4 and dev4 is not None:
+            dev, pl = dev4, pl4
+        else:
+            dev = torch.from_numpy(D.generate(D.spec(cfg))).to(stream.device)
+            pl = Pipeline(D.params(cfg), device=stream.device.index)
+            pl.set_stream(stream.cuda_stream)
+        n = dev.shape[0]
+        g = torch.Generator(device=dev.device)
+        g.manual_seed(11)
+        for order in ("gen", "shuffled"):
+            x = dev if order == "gen" else dev[torch.randperm(n, device=dev.device, generator=g)]
+            for _ in range(max(3, args.warmup)):
+                pl.run(x)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            k1 = []
+            e0.record(stream)
+            for _ in range(args.steps):
+                k1.append(pl.run(x).ms_contract)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            k1_ms = statistics.mean(k1)
+            out[f"config{cfg}_{order}"] = {
+                "points": n, "ms_per_step": ms, "points_per_s": n / (ms / 1e3),
+                "roofline_frac": (BYTES_PER_POINT * n / (ms / 1e3) / 1e9) / peak,
+                "contract_ms": k1_ms,
+                "contract_frac": (BYTES_PER_POINT * n / (k1_ms / 1e3) / 1e9) / peak}
+            del x
+        del dev
+    return out
 
 
 def ours(args) -> None:
@@ -366,6 +444,9 @@ def ours(args) -> None:
                              "order": "torch.randperm(seed 11) on the device"}
         del shuf
 
+    if not args.quick and world == 1:
+        extra["per_config"] = per_config_sweep(args, pl, stream, dev if cfg == 4 else None)
+
     peak, peak_src = measured_peak_gbs()
     k1_ms = statistics.mean(ms_contract)
     achieved = BYTES_PER_POINT * n / (k1_ms / 1e3) / 1e9
@@ -401,8 +482,9 @@ def ours(args) -> None:
     if extra:
         line["extra"] = extra
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_sample = min(n, args.cpu_sample)
-        line["cpu_baseline"] = cpu_baseline_sequential(host.numpy(), gp, n_sample)
+        n_count = min(n, args.cpu_sample) if args.cpu_sample else n
+        n_retain = min(n, args.cpu_retain_sample)
+        line["cpu_baseline"] = cpu_baseline_sequential(host.numpy(), gp, n_count, n_retain)
     if rank == 0:
         print(json.dumps(line))
     if dist:
@@ -418,8 +500,14 @@ def main() -> None:
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--order", choices=["gen", "shuffled"], default="gen")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-sample", type=int, default=20_000_000)
-    ap.add_argument("--ref-sample", type=int, default=20_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="points for the 1-core count-mode baseline (0: the whole workload)")
+    ap.add_argument("--cpu-retain-sample", type=int, default=50_000_000,
+                    help="points for the 1-core Mode::retain_points baseline (0: skip)")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="points for the reference arm (0: the whole workload)")
+    ap.add_argument("--ref-budget-s", type=float, default=1000.0,
+                    help="time budget of the reference arm's timed runs")
     ap.add_argument("--ref-workers", type=int, default=None)
     ap.add_argument("--quick", action="store_true", help="skip the labelled-variant extra")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")

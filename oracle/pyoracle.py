@@ -100,6 +100,10 @@ def ref():
                                           C.POINTER(C.c_uint64), C.POINTER(C.c_double),
                                           C.POINTER(C.c_double)]
         lib.ref_time_pipeline.restype = C.c_double
+        lib.ref_time_pipeline_mode.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.c_uint,
+                                               C.c_int, C.POINTER(C.c_uint64),
+                                               C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.ref_time_pipeline_mode.restype = C.c_double
         lib.ref_agglomerate.argtypes = [P, P, P, C.c_uint64, C.POINTER(orc_params),
                                         C.POINTER(orc_result)]
         lib.ref_cluster_flags.argtypes = [P, C.c_uint64, C.POINTER(orc_params), C.c_int,
@@ -253,6 +257,20 @@ def ref_time(points_ptr: int, n: int, gp, workers: int = 0):
     tp, tc = C.c_double(), C.c_double()
     t = lib.ref_time_pipeline(points_ptr, n, C.byref(make_params(gp)), workers, C.byref(nc),
                               C.byref(tp), C.byref(tc))
+    if t < 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    return t, tp.value, tc.value, nc.value
+
+
+def ref_time_mode(points_ptr: int, n: int, gp, workers: int = 0, retain: bool = False):
+    """ref_time with Mode::retain_points when `retain` (the reference's
+    point-retaining pipeline); returns (t_total, t_projection, t_clustering,
+    n_clusters)."""
+    lib = ref()
+    nc = C.c_uint64()
+    tp, tc = C.c_double(), C.c_double()
+    t = lib.ref_time_pipeline_mode(points_ptr, n, C.byref(make_params(gp)), workers, int(retain),
+                                   C.byref(nc), C.byref(tp), C.byref(tc))
     if t < 0:
         raise RuntimeError(lib.ref_last_error().decode())
     return t, tp.value, tc.value, nc.value

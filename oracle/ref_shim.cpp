@@ -158,6 +158,32 @@ double ref_time_pipeline(const double* xy, uint64_t n, const orc_params* p, unsi
     }
 }
 
+// ref_time_pipeline with a mode: retain != 0 runs Mode::retain_points
+// (core.hpp:74; RASTER', every in-bounds point of a kept tile is stored,
+// accumulator.hpp:131) — the reference's form of the point-retaining variant.
+double ref_time_pipeline_mode(const double* xy, uint64_t n, const orc_params* p, unsigned workers,
+                              int retain, uint64_t* n_clusters, double* t_projection,
+                              double* t_clustering) {
+    try {
+        raster::GridParams params = to_params(p);
+        if (retain) params.mode = raster::Mode::retain_points;
+        std::span<const raster::Point> pts(reinterpret_cast<const raster::Point*>(xy), n);
+        raster::PipelineStats st;
+        raster::ClusterSet cs =
+            workers == 0
+                ? raster::cluster_sequential(pts, params, false, &st)
+                : raster::cluster_parallel(pts, params, raster::ParallelConfig{workers}, false,
+                                           &st);
+        if (n_clusters) *n_clusters = cs.clusters.size();
+        if (t_projection) *t_projection = st.t_projection;
+        if (t_clustering) *t_clustering = st.t_clustering;
+        return st.t_total;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1.0;
+    }
+}
+
 // agglomerate(SignificantTiles, params) over caller tiles.
 int ref_agglomerate(const int64_t* tx, const int64_t* ty, const uint64_t* count, uint64_t n,
                     const orc_params* p, orc_result* out) {

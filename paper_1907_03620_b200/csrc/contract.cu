@@ -10,13 +10,20 @@
 // prefetched one segment ahead so the atomic's latency is hidden), so hot
 // spots (config 5's blob) and cold regions load-balance dynamically.
 //
-// Aggregation. Per row the warp groups equal keys with __match_any_sync; each
-// distinct key's leader lane merges the group's count into a per-warp
-// direct-mapped write-back cache in shared memory (128 entries; slot
-// ownership per row is arbitrated through a shared-memory owner byte, so no
-// shared-memory atomics are needed). Entries reach the HBM table only when
-// evicted or at the end, so a run of points from one cluster costs one global
-// RED per distinct tile rather than one per point.
+// Staging. Each warp keeps a ring of rows in flight with per-lane 16-byte
+// cp.async copies (L2 evict-first). A TMA bulk-copy ring (one elected lane,
+// one cp.async.bulk + mbarrier per 2-row stage) is built too (RG_K1=tma);
+// it measured slower (K1).
+//
+// Aggregation. Every lane looks its tile up in a per-warp direct-mapped
+// write-back cache in shared memory (128 entries, slot = position in an
+// 8 x 16-tile window, so the tiles of one cluster never evict each other); a
+// hit is one shared-memory increment. Misses of a whole batch of rows are
+// resolved together: one missing point per slot wins it (owner byte),
+// evicts the old entry into a staging list and installs its tile; the
+// staging list is written to the HBM table 32 entries at a time by the
+// whole warp (CAS-first claims, RED adds). A run of points from one cluster
+// therefore costs about one global update per distinct tile.
 //
 // Growth without a device-side rehash in the loop. The reference grows its
 // table at 70% load (accumulator.hpp:34,84-94). Here each launch gives every
@@ -26,6 +33,9 @@
 // resumes exactly the unprocessed rows, so results are identical to a single
 // pass regardless of how often the table grew.
 #include <cub/device/device_radix_sort.cuh>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
@@ -65,21 +75,17 @@ struct K1Params {
 // Staging list: flushed once more than kStageCap - 32 entries wait (a row
 // adds at most 32).
 #ifndef RG_K1_STAGE
-#define RG_K1_STAGE 64
+#define RG_K1_STAGE (64 + 32 * RG_K1_BATCH)
 #endif
 constexpr u32 kStageCap = RG_K1_STAGE;
 
-#ifdef RG_K1_MATCH
-typedef u64 CacheCount;
-#else
 typedef u32 CacheCount;  // bounded by the per-segment overflow check in k_contract
-#endif
 
 struct WarpSmem {
     u64 ckey[kCacheSlots];          // direct-mapped write-back cache: cache keys
     CacheCount ccnt[kCacheSlots];   //                                 counts
     u64 skey[kStageCap];     // staged (table key, count) pairs bound for the HBM table
-    u64 scnt[kStageCap];
+    u32 scnt[kStageCap];     // (cache counts stay below 2^31 + 8192, see k_contract)
     unsigned char owner[kCacheSlots];
 };
 
@@ -118,7 +124,7 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
     __syncwarp();
 }
 
-#ifndef RG_K1_MATCH
+#ifdef RG_K1_ROWWISE
 // One batch of kBatch rows already in registers (one point per lane per
 // row). Every lane looks its tile up in the per-warp cache; a hit adds 1
 // with a shared-memory reduction (fire-and-forget: the warp does not wait,
@@ -181,68 +187,135 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
             s.slen += ns;
             s.pot += ns;
             __syncwarp();
-            if (s.slen > kStageCap - 32) flush_stage(t, w, s, lane);
+            if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
         }
     }
 }
 #else
 // One batch of kBatch rows already in registers (one point per lane per
-// row). Keys and match masks of all rows are formed first so their
-// latencies overlap; rows are then merged into the cache in order (a later
-// row's hit must see an earlier row's install).
+// row). Every lane looks its tiles up in the per-warp cache; a hit adds 1
+// with a shared-memory increment (fire-and-forget: the warp does not wait,
+// and lanes of one tile are aggregated in the shared-memory atomic unit).
+// The lookups are branch-free (the slot of an out-of-bounds point is a
+// valid index, its kEmpty key never hits). Misses of ALL rows of the batch
+// are then resolved together, per slot: one missing (lane, row) wins the
+// slot, evicts the old occupant into the staging list (or leaves a
+// placeholder if the slot was empty) and installs its key with count 0;
+// every missing point whose key now owns its slot adds 1, the others stage
+// (key, 1). Each winner and each loser adds one staged entry.
 template <bool kNarrow>
 __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
                                               int lane, u32 lt_mask) {
     using K = KeyOps<kNarrow>;
     u64 key[kBatch];
-    u32 peers[kBatch];
+    u32 cs[kBatch];
+    bool miss[kBatch];
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) key[b] = K::cache_key(g, x[b], y[b]);
+    for (int r = 0; r < kBatch; ++r) {
+        key[r] = K::cache_key(g, x[r], y[r]);
+        cs[r] = K::slot(key[r], g.bits_y);
+    }
+    bool any = false;
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) peers[b] = match_any64(key[b]);
+    for (int r = 0; r < kBatch; ++r) {
+        const u64 ck = w.ckey[cs[r]];
+        const bool valid = key[r] != kEmpty;
+        const bool hit = (ck == key[r]) & valid;
+        if (hit) atomicAdd(&w.ccnt[cs[r]], 1u);
+        miss[r] = valid & !hit;
+        any |= miss[r];
+    }
+    if (!__any_sync(kFull, any)) return;
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-        // the group's lowest lane leads; out-of-bounds lanes never do
-        const bool leader = key[b] != kEmpty && (peers[b] & lt_mask) == 0;
-        const u32 cs = K::slot(key[b], g.bits_y);
-        const u32 cnt = __popc(peers[b]);
-        // Hit: the slot holds this key. Distinct keys never hit the same
-        // slot, so hitting leaders add without arbitration.
-        const bool hit = leader && w.ckey[cs] == key[b];
-        if (hit) w.ccnt[cs] += cnt;
-        const bool miss = leader && !hit;
-        const u32 missmask = ballot(miss);
-        if (missmask) {
-            // One missing leader per slot installs its key; every missing
-            // leader reserves a staging entry for what it displaces: the
-            // slot's old occupant (winner) or its own group (losers). A
-            // winner that found the slot empty leaves a placeholder. Each
-            // miss therefore adds one to (cache entries + staged entries).
-            if (miss) w.owner[cs] = (unsigned char)lane;
-            __syncwarp();
-            if (miss) {
-                u64 sk = K::table_key(key[b], g.bits_y), sc = cnt;
-                if (w.owner[cs] == lane) {
-                    sk = K::table_key(w.ckey[cs], g.bits_y);
-                    sc = w.ccnt[cs];
-                    w.ckey[cs] = key[b];
-                    w.ccnt[cs] = cnt;
-                }
-                const u32 pos = s.slen + __popc(missmask & lt_mask);
-                w.skey[pos] = sk;
-                w.scnt[pos] = sc;
-            }
-            const u32 nm = __popc(missmask);
-            s.slen += nm;
-            s.pot += nm;
-            __syncwarp();
-            if (s.slen > kStageCap - 32) flush_stage(t, w, s, lane);
+    for (int r = 0; r < kBatch; ++r)
+        if (miss[r]) w.owner[cs[r]] = (unsigned char)(r * 32 + lane);
+    __syncwarp();
+    u64 sk[kBatch];
+    u32 sc[kBatch];
+    bool win[kBatch];
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+        win[r] = miss[r] && w.owner[cs[r]] == (unsigned char)(r * 32 + lane);
+        sk[r] = kEmpty;
+        sc[r] = 0;
+        if (win[r]) {
+            sk[r] = K::table_key(w.ckey[cs[r]], g.bits_y);  // kEmpty: placeholder
+            sc[r] = w.ccnt[cs[r]];
+            w.ckey[cs[r]] = key[r];
+            w.ccnt[cs[r]] = 0;
         }
     }
+    __syncwarp();
+    u32 pos = s.slen;
+#pragma unroll
+    for (int r = 0; r < kBatch; ++r) {
+        bool lose = false;
+        if (miss[r]) {
+            if (w.ckey[cs[r]] == key[r]) {
+                atomicAdd(&w.ccnt[cs[r]], 1u);
+            } else {
+                lose = true;
+                sk[r] = K::table_key(key[r], g.bits_y);
+                sc[r] = 1;
+            }
+        }
+        const bool stage = win[r] | lose;
+        const u32 m = ballot(stage);
+        if (stage) {
+            const u32 at = pos + __popc(m & lt_mask);
+            w.skey[at] = sk[r];
+            w.scnt[at] = sc[r];
+        }
+        pos += __popc(m);
+    }
+    s.pot += pos - s.slen;
+    s.slen = pos;
+    __syncwarp();
+    if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
 }
+#endif  // RG_K1_ROWWISE
 
-#endif  // RG_K1_MATCH
+
+// ------------------------------------------------------- TMA bulk staging
+// One elected lane arms a stage's mbarrier with the byte count and issues
+// ONE bulk copy (cp.async.bulk, the TMA's non-tensor form, L2 evict-first)
+// for the whole stage; the warp waits on the mbarrier phase. This replaces
+// 32 per-lane LDGSTS + commit/wait per row.
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+    return (u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, u32 bytes, u64* bar,
+                                          u64 pol) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+#ifndef RG_MBAR_HINT
+#define RG_MBAR_HINT 0x989680
+#endif
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    // the suspend-time hint lets the scheduler park the warp until the phase
+    // completes instead of spinning on the barrier (issue slots)
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(RG_MBAR_HINT)
+        : "memory");
+}
 
 #ifndef RG_K1_RING
 #define RG_K1_RING 4
@@ -305,10 +378,65 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
     return nr;
 }
 
-template <bool kAligned, bool kNarrow>
+// run_segment with TMA bulk staging (16-byte aligned points): the ring is
+// kStages stages of kBatch rows; lane 0 refills a stage with one bulk copy
+// once every lane has read it. `phase` carries the stages' mbarrier parities
+// across segments. Same return convention as run_segment.
+constexpr int kStages = kRing / kBatch;
+template <bool kNarrow>
+__device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 valid,
+                                               double2 (*ring)[32], u64* bar, u32& phase,
+                                               const Grid& g, const Table& t, WarpSmem& w,
+                                               K1State& st, int lane, u32 lt_mask, u64 pol,
+                                               u32 budget) {
+    const u32 nb = (nr + kBatch - 1) / kBatch;
+    auto issue = [&](u32 b) {  // lane 0 only
+        const u32 first = b * (kBatch * 32);
+        const u32 cnt = min((u32)(kBatch * 32), valid - first);
+        bulk_load(ring[(b % kStages) * kBatch], src + first, cnt * 16u, &bar[b % kStages], pol);
+    };
+    if (lane == 0)
+        for (u32 b = 0; b < (u32)kStages && b < nb; ++b) issue(b);
+    u32 done_b = nb;
+    for (u32 b = 0; b < nb; ++b) {
+        const u32 s = b % kStages;
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+        double x[kBatch], y[kBatch];
+#pragma unroll
+        for (int r = 0; r < kBatch; ++r) {
+            const u32 idx = b * (kBatch * 32) + r * 32 + lane;
+            const double2 v = ring[s * kBatch + r][lane];
+            x[r] = idx < valid ? v.x : __longlong_as_double(0x7ff8000000000000ll);
+            y[r] = v.y;
+        }
+        __syncwarp();  // every lane has read the stage: it may be refilled
+        if (lane == 0 && b + kStages < nb) {
+#ifndef RG_K1_NOFENCE
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+            issue(b + kStages);
+        }
+        process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask);
+        if (st.pot >= budget) {
+            done_b = b + 1;
+            break;
+        }
+    }
+    // stages still in flight after a budget stop
+    for (u32 b = done_b; b < nb && b < done_b + kStages; ++b) {
+        const u32 s = b % kStages;
+        mbar_wait(&bar[s], (phase >> s) & 1u);
+        phase ^= 1u << s;
+    }
+    return done_b < nb ? done_b * kBatch : nr;
+}
+
+template <bool kAligned, bool kNarrow, bool kTma>
 __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ WarpSmem s_warp[kWarpsPerBlock];
     __shared__ __align__(16) double2 s_ring[kWarpsPerBlock][kRing][32];
+    __shared__ u64 s_bar[kWarpsPerBlock][kStages];
 
     const int lane = threadIdx.x & 31;
     const u32 lt_mask = (1u << lane) - 1;
@@ -317,6 +445,12 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
     for (int i = lane; i < kCacheSlots; i += 32) {
         w.ckey[i] = kEmpty;
         w.ccnt[i] = 0;
+    }
+    u64* bar = s_bar[threadIdx.x >> 5];
+    u32 phase = 0;
+    if (kTma && lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+        mbar_fence_init();
     }
     __syncwarp();
 
@@ -371,7 +505,6 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         const u64 row_end = min((seg + 1) * P.rows_per_seg, P.n_rows);
         if (lane == 0 && (from_ticket || P.n_partial_in == 0))
             pending = atomicAdd(&P.ctr->ticket, 1ull);
-#ifndef RG_K1_MATCH
         // 32-bit cache counts: a segment adds at most 32 * rows_per_seg
         // (<= 8192) to an entry, so moving large counts out here keeps
         // every entry below 2^31 + 8192.
@@ -389,20 +522,22 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
             st.pot += __reduce_add_sync(kFull, gc);  // the entry stays cached too
             __syncwarp();
         }
-#endif
         const u32 nr = (u32)(row_end - row0);
         const u64 p0 = row0 * 32;
         const u32 valid = (u32)min(P.n - p0, (u64)nr * 32);
         const double2* base = pts + p0 + lane;
         const double* xy_base = P.xy + 2 * p0;
         u32 done;
-        if (valid == nr * 32 && nr % kBatch == 0)
+        if (kTma)
+            done = run_segment_tma<kNarrow>(pts + p0, nr, valid, ring, bar, phase, g, t, w, st,
+                                            lane, lt_mask, pol, P.budget);
+        else if (valid == nr * 32 && nr % kBatch == 0)
             done = run_segment<kAligned, kNarrow, true>(base, xy_base, nr, valid, ring, g, t, w,
                                                         st, lane, lt_mask, pol, P.budget);
         else
             done = run_segment<kAligned, kNarrow, false>(base, xy_base, nr, valid, ring, g, t, w,
                                                          st, lane, lt_mask, pol, P.budget);
-        cp_async_wait<0>();
+        if (!kTma) cp_async_wait<0>();
         n_valid += min((u64)done * 32, (u64)valid);
         if (done < nr || st.pot >= P.budget) {
             if (done < nr) record_partial(seg, row0 + done);
@@ -746,13 +881,14 @@ static int g_k1_warps_per_sm = 0;
 // overshoot its load target (see ingest_device in api.cu).
 int contract_max_warps(int n_sm) {
     if (!g_k1_warps_per_sm) {
-        int b[4] = {0, 0, 0, 0};
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_contract<true, true>, kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_contract<true, false>, kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_contract<false, true>, kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_contract<false, false>, kThreads, 0);
+        int b[5] = {0, 0, 0, 0, 0};
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_contract<true, true, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_contract<true, false, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_contract<false, true, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_contract<false, false, false>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[4], k_contract<true, true, true>, kThreads, 0);
         int m = b[0];
-        for (int i = 1; i < 4; ++i) m = b[i] < m ? b[i] : m;
+        for (int i = 1; i < 5; ++i) m = b[i] < m ? b[i] : m;
         g_k1_warps_per_sm = (m < 1 ? 1 : m) * kWarpsPerBlock;
     }
     return g_k1_warps_per_sm * n_sm;
@@ -777,14 +913,22 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     P.budget = (u32)(L.budget < (1ull << 30) ? L.budget : (1ull << 30));
     const int blocks = (int)((L.warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const bool aligned = ((uintptr_t)L.xy & 15) == 0;
-    if (aligned && L.narrow)
-        k_contract<true, true><<<blocks, kThreads, 0, st>>>(P);
+    // RG_K1=tma selects the TMA bulk-copy ring (measured slower than the
+    // per-lane cp.async ring: DESIGN.md, K1)
+    static const bool tma = [] {
+        const char* v = std::getenv("RG_K1");
+        return v && std::strcmp(v, "tma") == 0;
+    }();
+    if (aligned && L.narrow && tma)
+        k_contract<true, true, true><<<blocks, kThreads, 0, st>>>(P);
+    else if (aligned && L.narrow)
+        k_contract<true, true, false><<<blocks, kThreads, 0, st>>>(P);
     else if (aligned)
-        k_contract<true, false><<<blocks, kThreads, 0, st>>>(P);
+        k_contract<true, false, false><<<blocks, kThreads, 0, st>>>(P);
     else if (L.narrow)
-        k_contract<false, true><<<blocks, kThreads, 0, st>>>(P);
+        k_contract<false, true, false><<<blocks, kThreads, 0, st>>>(P);
     else
-        k_contract<false, false><<<blocks, kThreads, 0, st>>>(P);
+        k_contract<false, false, false><<<blocks, kThreads, 0, st>>>(P);
     return cudaGetLastError();
 }
 
