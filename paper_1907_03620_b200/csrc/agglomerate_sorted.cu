@@ -453,39 +453,236 @@ __global__ void k_sorted_reduce(u32* parent, const u32* perm, const u64* cnt_b,
 // inside the id scan: the root of a component is its smallest tile, so the
 // exclusive scan of the flags in sorted order is the canonical id
 // (finalize_clusters agglomerate.hpp:186-190).
-struct KeptRoot {
-    const u32* parent;
-    const u32* size;
-    u64 mu;
-    __host__ __device__ u32 operator()(u32 i) const { return parent[i] == i && size[i] >= mu; }
-};
-using KeptIter = thrust::transform_iterator<KeptRoot, thrust::counting_iterator<u32>>;
 
 
-// Canonical ids: id of a tile = scan value at its root (when the root is
-// kept); scattered to bucket order for the labelling pass; cluster k's root
-// recorded for cluster facts; roots counted.
-__global__ void k_sorted_label(const u32* parent, const u32* size, u64 mu, const u32* scan,
-                               const u32* perm, const u64* n_sig_p, int* tile_cid_b,
-                               int* cid_s, u32* clu_root, Counters* ctr) {
-    const u64 n = *n_sig_p;
-    u32 roots = 0;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x) {
-        u32 r = parent[i], nx;
-        while ((nx = s_ld_parent(parent + r)) != r) r = nx;  // linked bucket roots (P3)
-        const bool kept = size[r] >= mu;
-        const int cid = kept ? (int)scan[r] : -1;
-        cid_s[i] = cid;
-        if (tile_cid_b) tile_cid_b[perm[i]] = cid;  // null: scattered on demand (api.cu)
-        if (r == (u32)i) {
-            ++roots;
-            if (kept) clu_root[cid] = (u32)i;
-        }
-        if (i == n - 1) ctr->n_kept = (u64)scan[i] + (r == (u32)i && kept ? 1u : 0u);
+
+// ---------------------------------------------------- single-pass scans
+// Decoupled look-back (one pass, no library scan): a block takes the next
+// tile from a ticket, publishes its aggregate, reads its predecessors'
+// published values back to the first inclusive prefix, and publishes its
+// own inclusive prefix. Status word: flag (2 bits) << 62 | value.
+constexpr u64 kLbAgg = 1ull << 62, kLbPre = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_store(u64* p, u64 v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 lb_load(const u64* p) {
+    u64 v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Called by one whole warp: the exclusive prefix of `tile` given its
+// aggregate. The warp inspects 32 predecessors at a time (each lane waits
+// until its predecessor has published something), adds up aggregates back to
+// the nearest inclusive prefix, and publishes its own inclusive prefix.
+__device__ __forceinline__ u64 lb_prefix(u64* status, u32 tile, u64 agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) lb_store(status, kLbPre | agg);
+        return 0;
     }
-    const u32 w = __reduce_add_sync(kFull, roots);
-    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&ctr->n_roots, (u64)w);
+    if (lane == 0) lb_store(status + tile, kLbAgg | agg);
+    u64 pre = 0;
+    for (long long j = (long long)tile - 1;; j -= 32) {
+        const long long idx = j - lane;
+        u64 v = kLbPre;  // before tile 0: an inclusive prefix of 0
+        if (idx >= 0)
+            while (((v = lb_load(status + idx)) >> 62) == 0) {
+            }
+        const u32 pm = __ballot_sync(kFull, (v >> 62) == 2);
+        // lanes up to the nearest inclusive prefix (all 32 when none)
+        const int last = pm ? __ffs(pm) - 1 : 31;
+        u64 x = lane <= last ? (v & kLbVal) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        pre += x;
+        if (pm) break;
+    }
+    if (lane == 0) lb_store(status + tile, kLbPre | (pre + agg));
+    return pre;
+}
+
+// Block-wide exclusive sum of one u32 per thread (kThr threads); the block
+// total through *total.
+template <int kThr>
+__device__ __forceinline__ u32 block_excl_sum(u32 v, u32* s_warp, u32* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const u32 w = lane < kThr / 32 ? s_warp[lane] : 0;
+        u32 wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(kFull, wi, d);
+            if (lane >= d) wi += y;
+        }
+        if (lane < kThr / 32) s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    *total = s_warp[32];
+    return s_warp[wid] + incl - v;
+}
+
+// Column offsets for the column-ordered K3 in one pass (replaces a column
+// maximum pass, a library scan and a bucket-bounds search): col_off =
+// exclusive scan of the column histogram (cols + 1 entries, the last is n),
+// the longest column into *max_col, and for 2^shift-tile buckets the start
+// of bucket b, rs[b] = the first column start >= b << shift (rs[nbkt] = n),
+// copied to the scatter cursors rs[nbkt + 1 + b]. One block per tile.
+constexpr int kCsThr = 256, kCsPer = 16, kCsTile = kCsThr * kCsPer;
+__global__ void __launch_bounds__(kCsThr) k_col_scan(const u32* cnt, u64 cols, const u64* n_p,
+                                                     u32 shift, u32* col_off, u32* max_col,
+                                                     u32* rs, u64* status, u32* ticket) {
+    __shared__ u32 s_warp[33];
+    __shared__ u32 s_tile;
+    __shared__ u64 s_pre;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 total_cols = cols + 1;
+    const u64 c0 = (u64)tile * kCsTile + (u64)threadIdx.x * kCsPer;
+    u32 v[kCsPer];
+    u32 sum = 0, mx = 0;
+#pragma unroll
+    for (int j = 0; j < kCsPer; ++j) {
+        v[j] = c0 + j < cols ? cnt[c0 + j] : 0;  // index cols is the end marker
+        sum += v[j];
+        mx = max(mx, v[j]);
+    }
+    u32 agg;
+    const u32 ex = block_excl_sum<kCsThr>(sum, s_warp, &agg);
+    if (threadIdx.x < 32) {
+        const u64 pre = lb_prefix(status, tile, agg);
+        if (threadIdx.x == 0) s_pre = pre;
+    }
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_col, mx);
+    __syncthreads();
+    const u64 n = *n_p;
+    const u64 nbkt = (n + (1ull << shift) - 1) >> shift;
+    u32* cur = rs + nbkt + 1;
+    u64 off = s_pre + ex;
+    // column c starts at s_c; bucket b starts at c when s_{c-1} < b << shift <= s_c
+    u64 prev = c0 > 0 && c0 - 1 < cols ? off - cnt[c0 - 1] : off;
+#pragma unroll
+    for (int j = 0; j < kCsPer; ++j) {
+        const u64 c = c0 + j;
+        if (c < total_cols) {
+            col_off[c] = (u32)off;
+            for (u64 b = c == 0 ? 0 : (prev >> shift) + 1; b < nbkt && (b << shift) <= off; ++b) {
+                rs[b] = (u32)off;
+                cur[b] = (u32)off;
+            }
+            if (c == cols) rs[nbkt] = (u32)n;
+        }
+        prev = off;
+        off += v[j];
+    }
+}
+
+// Canonical ids in one pass (replaces the kept-root library scan and the
+// labelling kernel): in sorted order a tile's root is its component's
+// smallest position (P2-P4 link larger roots under smaller ones), so the
+// number of kept roots before a root is its cluster id (finalize_clusters
+// agglomerate.hpp:186-190). Tiles whose root lies in an earlier tile wait
+// for that tile's ids (tiles are taken in ticket order: the wait ends).
+constexpr int kLbThr = 256, kLbPer = 16, kLbTile = kLbThr * kLbPer;
+__global__ void __launch_bounds__(kLbThr) k_sorted_ids(const u32* parent, const u32* size,
+                                                       u64 mu, const u32* perm, const u64* n_sig_p,
+                                                       int* tile_cid_b, int* cid_s, u32* clu_root,
+                                                       Counters* ctr, u64* status, u32* done,
+                                                       u32* ticket) {
+    __shared__ u32 s_warp[33];
+    __shared__ u32 s_tile;
+    __shared__ u64 s_pre;
+    __shared__ int s_cid[kLbTile];
+    __shared__ u32 s_root[kLbTile];
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const u64 n = *n_sig_p;
+    const u64 t0 = (u64)tile * kLbTile;
+    // roots (coalesced: item j of thread t is position t0 + j * kLbThr + t)
+#pragma unroll 4
+    for (int j = 0; j < kLbPer; ++j) {
+        const u32 li = j * kLbThr + threadIdx.x;
+        u32 r = 0xffffffffu;
+        if (t0 + li < n) {
+            // parent is final here (read-only in this kernel): cached loads
+            r = __ldg(parent + t0 + li);
+            u32 nx;
+            while ((nx = __ldg(parent + r)) != r) r = nx;  // linked bucket roots (P3)
+        }
+        s_root[li] = r;
+    }
+    __syncthreads();
+    // kept-root flags in position order: thread t owns positions t * kLbPer ..
+    u32 flags = 0, cntk = 0, roots = 0;
+#pragma unroll
+    for (int j = 0; j < kLbPer; ++j) {
+        const u32 li = threadIdx.x * kLbPer + j;
+        const bool root = t0 + li < n && s_root[li] == (u32)(t0 + li);
+        const bool kept = root && __ldg(size + t0 + li) >= mu;
+        flags |= (u32)kept << j;
+        cntk += kept;
+        roots += root;
+    }
+    u32 agg;
+    const u32 ex = block_excl_sum<kLbThr>(cntk, s_warp, &agg);
+    if (threadIdx.x < 32) {
+        const u64 pre = lb_prefix(status, tile, agg);
+        if (threadIdx.x == 0) s_pre = pre;
+    }
+    __syncthreads();
+    const u64 pre = s_pre;
+    u32 k = ex;
+#pragma unroll
+    for (int j = 0; j < kLbPer; ++j) {
+        const u32 li = threadIdx.x * kLbPer + j;
+        int cid = -1;
+        if ((flags >> j) & 1u) {
+            cid = (int)(pre + k++);
+            clu_root[cid] = (u32)(t0 + li);
+            cid_s[t0 + li] = cid;
+        }
+        s_cid[li] = cid;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(done + tile, 1u);  // this tile's root ids are visible
+    }
+#pragma unroll 4
+    for (int j = 0; j < kLbPer; ++j) {
+        const u32 li = j * kLbThr + threadIdx.x;
+        const u64 i = t0 + li;
+        if (i >= n) continue;
+        const u32 r = s_root[li];
+        int cid;
+        if (r >= t0) {
+            cid = s_cid[r - t0];
+        } else {  // root in an earlier tile: wait for its ids
+            const u32 rt = (u32)(r / kLbTile);
+            while (*(volatile u32*)(done + rt) == 0) {
+            }
+            __threadfence();
+            cid = __ldg(size + r) >= mu ? *(volatile int*)(cid_s + r) : -1;
+        }
+        cid_s[i] = cid;
+        if (tile_cid_b) tile_cid_b[perm[i]] = cid;
+    }
+    roots = __reduce_add_sync(kFull, roots);
+    if ((threadIdx.x & 31) == 0 && roots) atomicAdd(&ctr->n_roots, (u64)roots);
+    if (t0 + kLbTile >= n && threadIdx.x == 0) ctr->n_kept = pre + agg;  // the last tile
 }
 
 // Key sort by columns (when the column field has <= kColBitsMax bits): a
@@ -516,15 +713,6 @@ __global__ void k_col_hist(const u64* key, const u64* n_p, u32 bits_y, u32* cnt,
     }
     mx = __reduce_max_sync(kFull, mx);
     if (lane == 0 && mx) atomicMax(max_col, mx);
-}
-
-__global__ void k_col_max(const u32* cnt, u64 cols, u32* max_col) {
-    u32 mx = 0;
-    for (u64 c = blockIdx.x * (u64)blockDim.x + threadIdx.x; c < cols;
-         c += (u64)gridDim.x * blockDim.x)
-        mx = max(mx, cnt[c]);
-    mx = __reduce_max_sync(kFull, mx);
-    if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_col, mx);
 }
 
 // Each thread scatters kColIlp keys of a warp tile whose reservations are in
@@ -612,28 +800,6 @@ constexpr int kP2Items = 12;
 #endif
 constexpr u64 kBktMaxCol = RG_BKT_MAX_COL;  // 4096 + kBktMaxCol <= 512 * kP2Items
 constexpr size_t p2_smem(int threads) { return (size_t)threads * kP2Items * (8 + 4 + 4 + 2); }
-
-// rs[b] = first column start >= b * kBkt (lower bound in col_off), rs[nbkt] = n;
-// the scatter cursors start there.
-__global__ void k_bkt_bounds(const u32* col_off, u64 cols, u64 n, u32 nbkt, u32 shift, u32* rs,
-                             u32* cur) {
-    for (u64 b = blockIdx.x * (u64)blockDim.x + threadIdx.x; b <= nbkt;
-         b += (u64)gridDim.x * blockDim.x) {
-        u32 v = (u32)n;
-        if (b < nbkt) {
-            const u64 target = b << shift;
-            u64 lo = 0, hi = cols + 1;  // col_off has cols + 1 entries, col_off[cols] = n
-            while (lo < hi) {
-                const u64 m = (lo + hi) >> 1;
-                if ((u64)col_off[m] < target) lo = m + 1;
-                else hi = m;
-            }
-            v = lo <= cols ? col_off[lo] : (u32)n;
-            cur[b] = v;
-        }
-        rs[b] = v;
-    }
-}
 
 __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 n, u32 bits_y,
                                                             const u32* col_off, u32* cur,
@@ -963,12 +1129,6 @@ size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x) {
     cub::DeviceRadixSort::SortPairs((void*)nullptr, a, (const u64*)nullptr, (u64*)nullptr,
                                     (const u32*)nullptr, (u32*)nullptr, (int)n, 0, bits);
     cub::DeviceScan::ExclusiveSum((void*)nullptr, b, (const u32*)nullptr, (u32*)nullptr, (int)n);
-    {
-        size_t b2 = 0;
-        const KeptIter kept(thrust::counting_iterator<u32>(0), KeptRoot{nullptr, nullptr, 0});
-        cub::DeviceScan::ExclusiveSum((void*)nullptr, b2, kept, (u32*)nullptr, (int)n);
-        b = std::max(b, b2);
-    }
     const u64 cols = sorted_columns(bits_x);
     if (cols) {
         cub::DeviceScan::ExclusiveSum((void*)nullptr, c, (const u32*)nullptr, (u32*)nullptr,
@@ -978,7 +1138,24 @@ size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x) {
                                             (int)n, (int)cols, (const u32*)nullptr,
                                             (const u32*)nullptr);
     }
-    return std::max(std::max(a, b), std::max(c, d));
+    const u64 tiles = std::max<u64>((n + kLbTile - 1) / kLbTile, (cols + kCsTile) / kCsTile) + 1;
+    const size_t lb = 16 + tiles * 12;  // look-back scans: ticket, status words, done flags
+    return std::max(std::max(std::max(a, b), std::max(c, d)), lb);
+}
+
+// Look-back scratch at the start of the temp buffer, cleared before a scan.
+struct LbScratch {
+    u32* ticket;
+    u64* status;
+    u32* done;
+};
+static LbScratch lb_scratch(void* temp, u64 tiles, cudaStream_t st) {
+    LbScratch r;
+    r.ticket = (u32*)temp;
+    r.status = (u64*)((char*)temp + 16);
+    r.done = (u32*)(r.status + tiles);
+    cudaMemsetAsync(temp, 0, 16 + tiles * 12, st);
+    return r;
 }
 
 // Columns longer than this reach CUB's large-segment path, which sorts all 64
@@ -994,16 +1171,20 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     cudaError_t e;
     size_t bytes = L.temp_bytes;
     const u64 cols = sorted_columns(L.key_bits - L.bits_y);
+    constexpr u32 shift = 12;  // 4096-tile buckets
     if (cols && L.col_cnt) {
         cudaMemsetAsync(&L.ctr->max_col, 0, sizeof(u64), st);
-        if (L.col_hist_ready) {  // K2 built the histogram; only its maximum is missing
-            const int g = (int)std::min<u64>((cols + 255) / 256, (u64)L.n_sm * 8);
-            k_col_max<<<g, 256, 0, st>>>(L.col_cnt, cols, (u32*)&L.ctr->max_col);
-        } else {
+        if (!L.col_hist_ready) {  // (K2 builds the histogram on the prune path)
             cudaMemsetAsync(L.col_cnt, 0, (cols + 1) * sizeof(u32), st);
             k_col_hist<<<grid_for_s(L.n_sig, L.n_sm, 16), 256, 0, st>>>(
                 L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, (u32*)&L.ctr->max_col);
         }
+        // column offsets, longest column and bucket starts in one pass
+        const u64 tiles = (cols + kCsTile) / kCsTile;
+        const LbScratch lb = lb_scratch(L.temp, tiles, st);
+        k_col_scan<<<(int)tiles, kCsThr, 0, st>>>(L.col_cnt, cols, L.n_sig_dev, shift, L.col_off,
+                                                  (u32*)&L.ctr->max_col, L.flag, lb.status,
+                                                  lb.ticket);
     }
     // The exact significant count (L.n_sig may be an upper bound) and the
     // longest column decide the sort and size every launch below.
@@ -1017,19 +1198,12 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         std::fprintf(stderr, "[rg] K3 sorted: n=%llu max_col=%llu\n", (unsigned long long)n,
                      (unsigned long long)L.host_ctr->max_col);
     if (n == 0) {
-        if (L.launches) *L.launches = cols && L.col_cnt ? 1 : 0;
+        if (L.launches) *L.launches = cols && L.col_cnt ? (L.col_hist_ready ? 1 : 2) : 0;
         return cudaSuccess;
     }
     const int gs = grid_for_s(n, L.n_sm, 16);
-    int launches = cols && L.col_cnt ? 1 : 0;  // kernels launched (col_hist)
+    int launches = cols && L.col_cnt ? (L.col_hist_ready ? 1 : 2) : 0;  // col_hist, col_scan
     const u64 mcol = L.host_ctr->max_col;
-    // 4096-tile buckets by default; RG_BKT_SHIFT=11 selects 2048-tile buckets
-    // in 256-thread blocks (same P2 time, slower P1 on config 4)
-    static const bool small_bkt = [] {
-        const char* v = std::getenv("RG_BKT_SHIFT");
-        return v && std::atoi(v) == 11;
-    }();
-    const u32 shift = small_bkt && mcol <= 1024 && ((n + 2047) >> 11) * 8 <= 96 * 1024 ? 11 : 12;
     const u32 nbkt = (u32)((n + (1ull << shift) - 1) >> shift);
     const bool c1 = L.delta == 1 && !L.manhattan;
     bool bucket_counts = false;  // per-root counts already final (bucketed Chebyshev-1 path)
@@ -1039,12 +1213,10 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     }();
     if (cols && L.col_cnt && variant == 0 && mcol <= kBktMaxCol &&
         (size_t)nbkt * 8 <= 96 * 1024) {  // L.flag holds >= 1024 and >= n entries
-        // bucketed column sort (+ fused bucket-local unions for Chebyshev 1)
-        e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1), st);
-        if (e != cudaSuccess) return e;
+        // bucketed column sort (+ fused bucket-local unions for Chebyshev 1);
+        // k_col_scan left the bucket starts and the scatter cursors in flag
         u32* rs = L.flag;  // nbkt + 1 region starts, then nbkt scatter cursors
         u32* cur = L.flag + nbkt + 1;
-        k_bkt_bounds<<<(nbkt + 256) / 256, 256, 0, st>>>(L.col_off, cols, n, nbkt, shift, rs, cur);
         const size_t sm1 = (size_t)nbkt * 2 * sizeof(u32);
         static bool attr = false;
         if (!attr) {
@@ -1054,27 +1226,21 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(512));
             cudaFuncSetAttribute(k_bkt_sort<false, 512, 2>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(512));
-            cudaFuncSetAttribute(k_bkt_sort<true, 256, 4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(256));
-            cudaFuncSetAttribute(k_bkt_sort<false, 256, 4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p2_smem(256));
             attr = true;
         }
         const u64 t1 = (n + kP1Tile - 1) / kP1Tile;
         const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * (2048 / kP1Threads));
         k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, n, L.bits_y, L.col_off, cur, nbkt,
                                                    shift, L.ktmp, L.iota);
-        const bool small = shift == 11;
-        const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * (small ? 4 : 2));
+        const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * 2);
         auto p2 = [&](auto kernel, int threads) {
             kernel<<<g2, threads, p2_smem(threads), st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
                                                           L.bits_y, L.skey, L.perm, L.parent,
                                                           L.size);
         };
         if (c1) {
-            if (small) p2(k_bkt_sort<true, 256, 4>, 256);
-            else p2(k_bkt_sort<true, 512, 2>, 512);
-            launches += 5;  // scan (2), bounds, scatter, sort
+            p2(k_bkt_sort<true, 512, 2>, 512);
+            launches += 2;  // scatter, sort
             if (nbkt > 1) {
                 u32* linked = reinterpret_cast<u32*>(L.edges);  // >= 2n u32 entries
                 cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
@@ -1088,9 +1254,8 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
             bucket_counts = true;
             if (L.npts_deferred) *L.npts_deferred = true;
         } else {
-            if (small) p2(k_bkt_sort<false, 256, 4>, 256);
-            else p2(k_bkt_sort<false, 512, 2>, 512);
-            launches += 5;
+            p2(k_bkt_sort<false, 512, 2>, 512);
+            launches += 2;
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (!c1) {
@@ -1103,9 +1268,6 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         }
     } else {
         if (cols && L.col_cnt && variant != 2 && L.host_ctr->max_col <= kSegSortMaxColumn) {
-            e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, L.col_cnt, L.col_off, (int)(cols + 1),
-                                              st);
-            if (e != cudaSuccess) return e;
             cudaMemcpyAsync(L.col_cnt, L.col_off, (cols + 1) * sizeof(u32),
                             cudaMemcpyDeviceToDevice, st);
             k_col_scatter<<<gs, 256, 0, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_cnt, L.ktmp,
@@ -1115,7 +1277,7 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                                                     (int)n, (int)cols, L.col_off, L.col_off + 1,
                                                     st);
             if (e != cudaSuccess) return e;
-            launches += 7;  // scan (2), scatter, segmented sort (4)
+            launches += 5;  // scatter, segmented sort (4)
         } else {
             e = launch_iota(L.iota, n, L.n_sm, st);
             if (e != cudaSuccess) return e;
@@ -1140,13 +1302,14 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                                             L.npts, L.flag, L.mu);
         ++launches;
     }
-    bytes = L.temp_bytes;
-    const KeptIter kept(thrust::counting_iterator<u32>(0), KeptRoot{L.parent, L.size, L.mu});
-    e = cub::DeviceScan::ExclusiveSum(L.temp, bytes, kept, L.scan, (int)n, st);
-    if (e != cudaSuccess) return e;
-    k_sorted_label<<<gs, 256, 0, st>>>(L.parent, L.size, L.mu, L.scan, L.perm, L.n_sig_dev,
-                                       L.tile_cid_b, L.cid_s, L.clu_root, L.ctr);
-    launches += 3;  // scan (2), label
+    {
+        const u64 tiles = (n + kLbTile - 1) / kLbTile;
+        const LbScratch lb = lb_scratch(L.temp, tiles, st);
+        k_sorted_ids<<<(int)tiles, kLbThr, 0, st>>>(L.parent, L.size, L.mu, L.perm, L.n_sig_dev,
+                                                    L.tile_cid_b, L.cid_s, L.clu_root, L.ctr,
+                                                    lb.status, lb.done, lb.ticket);
+        launches += 1;
+    }
     if (L.launches) *L.launches = launches;
     return cudaGetLastError();
 }
