@@ -1188,11 +1188,20 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     }
     // The exact significant count (L.n_sig may be an upper bound) and the
     // longest column decide the sort and size every launch below.
-    if ((e = cudaMemcpyAsync(&L.host_ctr->n_sig, &L.ctr->n_sig,
-                             sizeof(Counters) - offsetof(Counters, n_sig),
-                             cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    if (L.check_k1_stop) {  // K1's counters ride along (its stop check was deferred)
+        if ((e = cudaMemcpyAsync(L.host_ctr, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost,
+                                 st)) != cudaSuccess)
+            return e;
+    } else if ((e = cudaMemcpyAsync(&L.host_ctr->n_sig, &L.ctr->n_sig,
+                                    sizeof(Counters) - offsetof(Counters, n_sig),
+                                    cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
         return e;
+    }
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if (L.check_k1_stop && L.host_ctr->stopped) {
+        if (L.launches) *L.launches = cols && L.col_cnt ? (L.col_hist_ready ? 1 : 2) : 0;
+        return cudaErrorNotReady;
+    }
     const u64 n = L.host_ctr->n_sig;
     if (std::getenv("RG_DEBUG"))
         std::fprintf(stderr, "[rg] K3 sorted: n=%llu max_col=%llu\n", (unsigned long long)n,

@@ -109,6 +109,8 @@ struct SortedLaunch {
     int n_sm;
     bool col_hist_ready;  // K2 already built col_cnt (prune_enqueue)
     bool* npts_deferred;  // out: per-cluster point totals left for launch_cluster_npts
+    bool check_k1_stop = false;  // the host read also checks K1's stop flag (returns
+                                 // cudaErrorNotReady, nothing launched after it, if set)
     int* launches;        // out: kernels launched
 };
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
