@@ -352,6 +352,11 @@ struct rg_ctx {
     u64 pair_cap = 0;
     u64 order_probe[3] = {0, 0, 0};
     u64 probe_fp = 0;       // fingerprint of the probed buffer's content
+    // K4' cell table of the kept tiles (labels of unordered inputs)
+    ulonglong2* lk_tab = nullptr;
+    int* lk_ids = nullptr;
+    u64 lk_cap = 0, lk_nb = 0, lk_ids_cap = 0;
+    bool lk_valid = false;
     bool fp_check = false;  // a fingerprint of the reused buffer is in ctr->pad2[0]
     int chunk_verdict = -1;  // host-span ingest: the first chunk's verdict for the rest
     const double* probe_ptr = nullptr;  // last probed buffer and its verdict
@@ -580,6 +585,7 @@ rg_status k1_finish(rg_ctx* ctx);
 // (accumulator.hpp:171-173: counts_.clear()). ingested/skipped are kept, as in
 // the reference.
 rg_status reopen_accumulator(rg_ctx* ctx) {
+    ctx->lk_valid = false;
     if (ctx->k1.active) {  // an ingest whose stop check never ran: finish it
         rg_status s = k1_finish(ctx);
         if (s != RG_OK) return s;
@@ -669,6 +675,8 @@ void resolve_contract_timer(rg_ctx* ctx) {
 // (partition.cu). RG_INGEST=k1 / =part forces a path; otherwise a probe of
 // 64 windows of 4096 consecutive points decides: when more than a quarter
 // of a window's points open a new tile, K1's per-warp cache cannot help.
+bool buffer_unordered(rg_ctx* ctx, const double* xy, u64 n);
+
 bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
     static const int forced = [] {
         const char* v = std::getenv("RG_INGEST");
@@ -680,6 +688,12 @@ bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
     if (forced == 2) return true;
     if (n < (1ull << 22)) return false;
     if (ctx->chunk_verdict >= 0) return ctx->chunk_verdict != 0;
+    return buffer_unordered(ctx, xy, n);
+}
+
+// The order probe (memoised per buffer, see below): true when consecutive
+// points rarely share tiles.
+bool buffer_unordered(rg_ctx* ctx, const double* xy, u64 n) {
     // The same buffer clustered again (a serving loop, the bench) reuses the
     // verdict without a host round trip. Its content is still fingerprinted
     // on the device; the fingerprint comes back with the counters at the
@@ -1169,6 +1183,7 @@ rg_status mark_table(rg_ctx* ctx, bool with_cids) {
 // K2 (+ window_fix / dedupe pre-passes) enqueued on the stream; the
 // significant count stays on the device (ctr->n_sig).
 rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
+    ctx->lk_valid = false;
     if (ctx->state != rg_ctx::kAccum) {
         // prune() on a consumed accumulator returns nothing (empty table).
         rg_status s = reopen_accumulator(ctx);
@@ -1655,6 +1670,8 @@ void rg_destroy(rg_ctx* ctx) {
     ctx->part_scratch = nullptr;
     dfree(ctx->pair_key);
     dfree(ctx->pair_cnt);
+    dfree(ctx->lk_tab);
+    dfree(ctx->lk_ids);
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {
@@ -2439,6 +2456,58 @@ rg_status rg_label_points(rg_ctx* ctx, const double* xy, uint64_t n, int32_t* la
             std::memset(labels, 0xff, n * sizeof(int32_t));
         }
         return RG_OK;
+    }
+    static const bool k4_table = [] {  // RG_K4=table: always the count-table lookups (A/B)
+        const char* v = std::getenv("RG_K4");
+        return v && std::strcmp(v, "table") == 0;
+    }();
+    if (kind == RG_MEM_DEVICE && ctx->sorted && ((uintptr_t)xy & 15) == 0 && ctx->narrow &&
+        !k4_table && n >= (1ull << 22) && buffer_unordered(ctx, xy, n)) {
+        // K4': no spatial order, so labels come from a cell table of the
+        // kept tiles (L2-sized) instead of the count table
+        const u32 kb = ctx->res.bits_x + ctx->res.bits_y;
+        if (kb <= 37 && ctx->res.bits_y >= 3 && ctx->n_kept < 0x7ffffff0ull) {
+            if (!ctx->lk_valid) {
+                if (ctx->lk_ids_cap < ctx->n_sig) {
+                    dfree(ctx->lk_ids);
+                    ctx->lk_ids_cap = 0;
+                    CK(dalloc(&ctx->lk_ids, std::max<u64>(ctx->n_sig, 1024)));
+                    ctx->lk_ids_cap = std::max<u64>(ctx->n_sig, 1024);
+                }
+                u64 cells = std::max<u64>(1024, ctx->n_sig / 4);  // grown below if more
+                u64* dctr = ctx->scratch + 4;
+                for (int attempt = 0;; ++attempt) {
+                    const u64 nb = cell_buckets(cells);
+                    if (ctx->lk_cap < nb) {
+                        dfree(ctx->lk_tab);
+                        ctx->lk_cap = 0;
+                        CK(dalloc(&ctx->lk_tab, 2 * nb));
+                        ctx->lk_cap = nb;
+                    }
+                    ctx->lk_nb = nb;
+                    CK(launch_cells_build(ctx->root_key_sorted, ctx->s_cid, &ctx->ctr->n_sig,
+                                          ctx->n_sig, ctx->lk_tab, nb, ctx->res.bits_y, dctr,
+                                          ctx->n_sm, ctx->st));
+                    ++ctx->launches;
+                    u64 h[2];
+                    CK(cudaMemcpyAsync(h, dctr, sizeof h, cudaMemcpyDeviceToHost, ctx->st));
+                    CK(cudaStreamSynchronize(ctx->st));
+                    if (!(u32)h[1]) break;
+                    if (attempt > 8) return set_err(ctx, RG_ERR_CUDA, "cell table did not fit");
+                    cells = std::max<u64>(cells * 2, h[0] * 2);  // every cell counted fits now
+                }
+                CK(launch_cells_mixed(ctx->root_key_sorted, ctx->s_cid, &ctx->ctr->n_sig,
+                                      ctx->n_sig, ctx->lk_tab, ctx->lk_nb, ctx->res.bits_y,
+                                      ctx->scratch + 4, ctx->lk_ids, ctx->n_sm, ctx->st));
+                ctx->launches += 2;
+                ctx->lk_valid = true;
+            }
+            CK(launch_label_cells(xy, n, ctx->grid, ctx->lk_tab, ctx->lk_nb, ctx->lk_ids, labels,
+                                  ctx->n_sm, ctx->st));
+            ++ctx->launches;
+            CK(cudaStreamSynchronize(ctx->st));
+            return RG_OK;
+        }
     }
     {
         rg_status ms = mark_table(ctx, true);

@@ -214,6 +214,18 @@ cudaError_t launch_cluster_points_v2_count(const PointsV2& L, cudaStream_t st, u
                                            u64* max_host);
 cudaError_t launch_cluster_points_v2(const PointsV2& L, u64 m, cudaStream_t st);
 
+// K4' for inputs without spatial order: a cell table of the kept tiles
+// (8 x 8-tile cells, 16-byte entries, L2-sized; label.cu)
+u64 cell_buckets(u64 cells);
+cudaError_t launch_cells_build(const u64* skey, const int* cid, const u64* n_dev, u64 n_bound,
+                               ulonglong2* tab, u64 nb, u32 bits_y, u64* counters, int n_sm,
+                               cudaStream_t st);
+cudaError_t launch_cells_mixed(const u64* skey, const int* cid, const u64* n_dev, u64 n_bound,
+                               ulonglong2* tab, u64 nb, u32 bits_y, u64* counters, int* ids,
+                               int n_sm, cudaStream_t st);
+cudaError_t launch_label_cells(const double* xy, u64 n, Grid g, const ulonglong2* tab, u64 nb,
+                               const int* ids, int* labels, int n_sm, cudaStream_t st);
+
 cudaError_t launch_label_points(const double* xy, u64 n, Grid g, Table t, const int* tile_cid,
                                 bool table_cids, int* labels, bool narrow, int n_sm,
                                 cudaStream_t st);

@@ -15,6 +15,8 @@
 // tile -> cluster id so only the first occurrence of a tile probes the HBM
 // table (whose value word holds SIG_BIT|index after K2). Labels are stored
 // coalesced.
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -131,6 +133,255 @@ __global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* 
         }
         cp_async_wait<0>();
     }
+}
+
+// ------------------------------------------- K4' (inputs without order)
+// With no spatial order every point misses the per-warp cache and probes
+// the HBM count table: a random sector of a table far larger than L2. Here
+// the labels come from a CELL table of the kept tiles, dense enough to stay
+// in L2 while the points stream past evict-first. A cell is 8 x 8 tiles;
+// its 16-byte entry holds the cell id, the cluster id of its kept tiles and
+// a 64-bit mask of which of its tiles are kept. A cell whose kept tiles
+// belong to several clusters (rare) points into a per-tile id array instead
+// (ids in mask order). Entries sit two to a 32-byte bucket; a point reads
+// its cell's home bucket (rarely the next), tests one mask bit, done.
+//   w0 = (cell id + 1) | info << 32, info = cluster id + 1, or kMixed | base
+//   w1 = kept-tile mask (bit = (kx & 7) * 8 + (ky & 7))
+constexpr u32 kMixed = 0x80000000u;
+constexpr int kCellBits = 3;
+
+__device__ __forceinline__ u64 cell_bucket(u32 cell, u64 nb) {
+    u64 h = (u64)cell * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31;
+    return __umul64hi(h, nb);
+}
+__device__ __forceinline__ u32 cell_of(u64 key, u32 bits_y) {
+    const u64 kx = key >> bits_y, ky = key & ((1ull << bits_y) - 1);
+    return (u32)(((kx >> kCellBits) << (bits_y - kCellBits)) | (ky >> kCellBits));
+}
+__device__ __forceinline__ u32 cell_bit(u64 key, u32 bits_y) {
+    return (u32)(((key >> bits_y) & 7) * 8 + (key & 7));
+}
+
+// Pass 1: insert every kept tile's cell and mask bit (cell ids are unique per
+// table, inserted with one CAS); a cell meeting a second cluster id is
+// flagged mixed. *n_cells counts cells; *over flags a table that filled up.
+__global__ void k_cells_build(const u64* skey, const int* cid, const u64* n_p, ulonglong2* tab,
+                              u64 nb, u32 bits_y, u64 cap_cells, u64* n_cells, u32* over) {
+    const u64 n = *n_p;
+    const int lane = threadIdx.x & 31;
+    const u64 span = (n + 31) / 32 * 32;  // whole warps: the aggregation below is warp-wide
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < span;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int c = i < n ? cid[i] : -1;
+        const u64 key = c >= 0 ? skey[i] : 0;
+        const u32 cell = cell_of(key, bits_y);
+        // tiles of one column and cell are consecutive in sorted order: one
+        // lane per (cell, cluster) group inserts the group's mask bits
+        const u64 tag = c >= 0 ? ((u64)cell << 32) | (u32)c : ~0ull;
+        const u32 peers = __match_any_sync(kFull, tag);
+        const u64 mine = c >= 0 ? 1ull << cell_bit(key, bits_y) : 0;
+        const u64 bits = (u64)__reduce_or_sync(peers, (u32)mine) |
+                         ((u64)__reduce_or_sync(peers, (u32)(mine >> 32)) << 32);
+        bool fresh = false;
+        if (c >= 0 && lane == __ffs(peers) - 1) {
+        const u64 want = (u64)(cell + 1) | ((u64)(u32)(c + 1) << 32);
+        u64 b = cell_bucket(cell, nb);
+        ulonglong2* e = nullptr;
+        for (u64 probes = 0; probes < nb && !e; ++probes) {
+#pragma unroll 1
+            for (int j = 0; j < 2; ++j) {
+                ulonglong2* q = tab + 2 * b + j;
+                u64 w0 = atomicCAS(&q->x, 0ull, want);
+                if (w0 == 0) {  // new cell
+                    fresh = true;
+                    e = q;
+                    break;
+                }
+                if ((u32)w0 == cell + 1) {
+                    if ((u32)(w0 >> 32) != (u32)(c + 1) && !((w0 >> 32) & kMixed))
+                        atomicOr(&q->x, (u64)kMixed << 32);
+                    e = q;
+                    break;
+                }
+            }
+            b = b + 1 == nb ? 0 : b + 1;
+        }
+        if (e)
+            atomicOr(&e->y, bits);
+        else
+            *over = 1;
+        }
+        // new cells counted once per warp (one counter would serialise)
+        const u32 nf = __popc(__ballot_sync(kFull, fresh));
+        if (lane == 0 && nf && atomicAdd(n_cells, (u64)nf) + nf > cap_cells) *over = 1;
+    }
+}
+
+// Pass 2: mixed cells get a base in the per-tile id array.
+__global__ void k_cells_mixed_base(ulonglong2* tab, u64 n_entries, u64* next) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_entries;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 w0 = tab[i].x;
+        if (!w0 || !((w0 >> 32) & kMixed)) continue;
+        const u64 base = atomicAdd(next, (u64)__popcll(tab[i].y));
+        tab[i].x = (w0 & 0xffffffffull) | ((u64)(kMixed | (u32)base) << 32);
+    }
+}
+
+__device__ __forceinline__ const ulonglong2* cell_find(const ulonglong2* tab, u64 nb, u32 cell,
+                                                       u64 pol);
+
+// Pass 3: kept tiles of mixed cells write their id at base + rank in mask.
+__global__ void k_cells_mixed_ids(const u64* skey, const int* cid, const u64* n_p,
+                                  const ulonglong2* tab, u64 nb, u32 bits_y, int* ids) {
+    const u64 n = *n_p;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int c = cid[i];
+        if (c < 0) continue;
+        const u64 key = skey[i];
+        const ulonglong2* e = cell_find(tab, nb, cell_of(key, bits_y), 0);
+        const u32 info = (u32)(e->x >> 32);
+        if (!(info & kMixed)) continue;
+        const u32 bit = cell_bit(key, bits_y);
+        ids[(info & ~kMixed) + __popcll(e->y & ((1ull << bit) - 1))] = c;
+    }
+}
+
+__device__ __forceinline__ void ld_entry(const ulonglong2* p, u64 pol, u64& a, u64& b) {
+    asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(a), "=l"(b)
+                 : "l"(p), "l"(pol));
+}
+
+// Cell entry or nullptr (build-time lookups use pol = 0: no hint needed).
+__device__ __forceinline__ const ulonglong2* cell_find(const ulonglong2* tab, u64 nb, u32 cell,
+                                                       u64) {
+    u64 b = cell_bucket(cell, nb);
+    while (true) {
+        bool open = false;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const u64 w0 = tab[2 * b + j].x;
+            if ((u32)w0 == cell + 1) return tab + 2 * b + j;
+            open |= w0 == 0;
+        }
+        if (open) return nullptr;
+        b = b + 1 == nb ? 0 : b + 1;
+    }
+}
+
+__device__ __forceinline__ void st_label_stream(int* p, int v) {
+    asm volatile("st.global.cs.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Resolves a cell entry pair for one point: 1 = found (label in c), 0 = the
+// search must go on, -1 = an empty entry ends it (no kept tile).
+__device__ __forceinline__ int cell_try(u64 a0, u64 m0, u64 a1, u64 m1, u32 cell, u32 bit,
+                                        const int* ids, int& c) {
+    u64 w = 0, m = 0;
+    if ((u32)a0 == cell + 1) {
+        w = a0;
+        m = m0;
+    } else if ((u32)a1 == cell + 1) {
+        w = a1;
+        m = m1;
+    }
+    if (w) {
+        if ((m >> bit) & 1) {
+            const u32 info = (u32)(w >> 32);
+            c = (info & kMixed) ? __ldg(ids + (info & ~kMixed) + __popcll(m & ((1ull << bit) - 1)))
+                                : (int)info - 1;
+        }
+        return 1;
+    }
+    return (!a0 || !a1) ? -1 : 0;
+}
+
+// Lookups of kLkIlp points per thread: the point loads are in flight
+// together; each lookup reads one 32-byte bucket (2 entries) and walks on
+// only when a full bucket does not hold the cell.
+constexpr int kLkIlp = 4;
+__global__ void __launch_bounds__(256) k_label_cells(const double2* xy, u64 n, Grid g,
+                                                     const ulonglong2* tab, u64 nb,
+                                                     const int* ids, int* labels) {
+    const u64 pol_pts = evict_first_policy();
+    u64 pol_tab;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_tab));
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 base = blockIdx.x * (u64)blockDim.x + threadIdx.x; base < n;
+         base += stride * kLkIlp) {
+        u64 key[kLkIlp];
+        bool ok[kLkIlp];
+#pragma unroll
+        for (int j = 0; j < kLkIlp; ++j) {
+            const u64 i = base + (u64)j * stride;
+            ok[j] = false;
+            key[j] = 0;
+            if (i < n) {
+                const double2 v = ld_point_stream(xy + i, pol_pts);
+                key[j] = pack_key(g, v.x, v.y);
+                ok[j] = in_bounds(g, v.x, v.y);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kLkIlp; ++j) {
+            const u64 i = base + (u64)j * stride;
+            if (i >= n) continue;
+            int c = -1;
+            if (ok[j]) {
+                const u32 cell = cell_of(key[j], g.bits_y), bit = cell_bit(key[j], g.bits_y);
+                u64 b = cell_bucket(cell, nb);
+                while (true) {
+                    u64 a0, m0, a1, m1;
+                    ld_entry(tab + 2 * b, pol_tab, a0, m0);
+                    ld_entry(tab + 2 * b + 1, pol_tab, a1, m1);
+                    if (cell_try(a0, m0, a1, m1, cell, bit, ids, c)) break;
+                    b = b + 1 == nb ? 0 : b + 1;
+                }
+            }
+            st_label_stream(labels + i, c);
+        }
+    }
+}
+
+u64 cell_buckets(u64 cells) { return std::max<u64>(16, (u64)((double)cells / (2 * 0.6)) + 1); }
+
+cudaError_t launch_cells_build(const u64* skey, const int* cid, const u64* n_dev, u64 n_bound,
+                               ulonglong2* tab, u64 nb, u32 bits_y, u64* counters, int n_sm,
+                               cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(tab, 0, nb * 32, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counters, 0, 3 * sizeof(u64), st);
+    if (e != cudaSuccess) return e;
+    const u64 want = (n_bound + 255) / 256;
+    const int blocks = (int)std::max<u64>(1, std::min<u64>(want, (u64)n_sm * 8));
+    // counters: [0] cells, [1] overflow flag, [2] mixed-id cursor
+    k_cells_build<<<blocks, 256, 0, st>>>(skey, cid, n_dev, tab, nb, bits_y,
+                                          (u64)((double)nb * 2 * 0.85), counters,
+                                          (u32*)(counters + 1));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cells_mixed(const u64* skey, const int* cid, const u64* n_dev, u64 n_bound,
+                               ulonglong2* tab, u64 nb, u32 bits_y, u64* counters, int* ids,
+                               int n_sm, cudaStream_t st) {
+    const u64 we = (nb * 2 + 255) / 256;
+    k_cells_mixed_base<<<(int)std::max<u64>(1, std::min<u64>(we, (u64)n_sm * 8)), 256, 0, st>>>(
+        tab, nb * 2, counters + 2);
+    const u64 want = (n_bound + 255) / 256;
+    k_cells_mixed_ids<<<(int)std::max<u64>(1, std::min<u64>(want, (u64)n_sm * 8)), 256, 0, st>>>(
+        skey, cid, n_dev, tab, nb, bits_y, ids);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_label_cells(const double* xy, u64 n, Grid g, const ulonglong2* tab, u64 nb,
+                               const int* ids, int* labels, int n_sm, cudaStream_t st) {
+    const u64 want = (n + 256 * kLkIlp - 1) / (256 * kLkIlp);
+    const int blocks = (int)std::max<u64>(1, std::min<u64>(want, (u64)n_sm * 8));
+    k_label_cells<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(xy), n, g, tab, nb, ids,
+                                          labels);
+    return cudaGetLastError();
 }
 
 static int g_label_blocks_per_sm = 0;

@@ -143,3 +143,27 @@ def test_order_verdict_follows_buffer_content():
     got = launches_of(pl, buf)
     assert abs(want_shuf - want_gen) > 2
     assert abs(got - want_shuf) <= 1, (got, want_shuf, want_gen)
+
+
+@pytest.mark.parametrize("cfg,scale", [(3, 0.1), (2, 1.0), (5, 0.05)])
+def test_labels_unordered_vs_oracle(cfg, scale):
+    """K4' (labels of inputs without spatial order: compact lookup of the
+    kept tiles) against the oracle's labeled_points, with out-of-bounds and
+    NaN points mixed in."""
+    import numpy as np
+    import torch
+
+    from oracle import pyoracle as O
+    from paper_1907_03620_b200 import datagen as D
+    from paper_1907_03620_b200.raster import Pipeline
+
+    gp = D.params(cfg)
+    pts = D.generate(D.spec(cfg, scale), shuffle_seed=13)
+    pts[::1009] = [500.0, 1.0]
+    pts[3::2003] = [np.nan, 0.5]
+    ref = O.port_cluster(pts, gp)
+    dev = torch.from_numpy(pts).cuda()
+    pl = Pipeline(gp)
+    pl.run(dev)
+    got = pl.label_points(dev).cpu().numpy()
+    assert np.array_equal(got, O.port_labels(pts, gp, ref))
