@@ -74,6 +74,15 @@ __device__ __forceinline__ u64 unmix(const Mix& m, u64 h) {
     return (h * m.inv) & m.mask;
 }
 
+// Point load that stays in L2 for a second read (KP1's placement pass).
+__device__ __forceinline__ double2 ld_point_keep(const double2* p, u64 pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ bool point_key(const Grid& g, double2 v, u64& key) {
     key = pack_key(g, v.x, v.y);
     return in_bounds(g, v.x, v.y);
@@ -162,14 +171,23 @@ __device__ __forceinline__ void block_scan_parts(const u32* in, u32* out, u32* w
 // round (histogram, then placement; the second read hits L2), so that each
 // partition's run of residuals averages 8 entries (one 32-byte sector) and
 // the O(partitions) bookkeeping is paid once per 16 Ki points.
-constexpr int kP1Thr = 1024;
+#ifndef RG_KP1_THREADS
+#define RG_KP1_THREADS 1024
+#endif
+#ifndef RG_KP1_STEPS
+#define RG_KP1_STEPS 2
+#endif
+#ifndef RG_KP1_BLOCKS
+#define RG_KP1_BLOCKS 1
+#endif
+constexpr int kP1Thr = RG_KP1_THREADS;
 constexpr u32 kP1SubN = kP1Thr * kPSub;  // points per pass step
-constexpr u32 kSubN = 2 * kP1SubN;
+constexpr u32 kSubN = RG_KP1_STEPS * kP1SubN;
 constexpr size_t kScatterSmem = (5 * kParts + kSubN + kP1Thr / 32) * 4 + kSubN * 2;
 static_assert(kParts % kP1Thr == 0 && kParts % kPThreads == 0, "partition scan layout");
 
 // KP1: every in-bounds point's residual, written at its partition's place.
-__global__ void __launch_bounds__(kP1Thr, 1) k_part_scatter(const double2* xy, u64 n, Grid g,
+__global__ void __launch_bounds__(kP1Thr, RG_KP1_BLOCKS) k_part_scatter(const double2* xy, u64 n, Grid g,
                                                             Mix m, const u32* off_pt, u64 T,
                                                             u32* res) {
     extern __shared__ u32 sh_sc[];  // kScatterSmem bytes
@@ -182,6 +200,8 @@ __global__ void __launch_bounds__(kP1Thr, 1) k_part_scatter(const double2* xy, u
     u32* wsum = stage + kSubN;
     unsigned short* spart = (unsigned short*)(wsum + kP1Thr / 32);
     const u64 pol = evict_first_policy();
+    u64 pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     for (u64 t = blockIdx.x; t < T; t += gridDim.x) {
         for (u32 p = threadIdx.x; p < kParts; p += kP1Thr) {
             cur[p] = off_pt[p * T + t];
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(kP1Thr, 1) k_part_scatter(const double2* xy, u
 #pragma unroll
                 for (int j = 0; j < kPSub; ++j) {
                     const u64 i = b + j * kP1Thr + threadIdx.x;
-                    v[j] = i < q1 ? xy[i]  // kept in L2 for pass b
+                    v[j] = i < q1 ? ld_point_keep(xy + i, pol_keep)  // kept in L2 for pass b
                                   : make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
                 }
 #pragma unroll
@@ -535,7 +555,7 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         cudaFuncSetAttribute(k_part_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
         attr = true;
     }
-    k_part_scatter<<<(int)std::min<u64>(T, (u64)L.n_sm), kP1Thr, kScatterSmem, st>>>(
+    k_part_scatter<<<(int)std::min<u64>(T, (u64)L.n_sm * RG_KP1_BLOCKS), kP1Thr, kScatterSmem, st>>>(
         xy, n, L.g, m, c.off, T, c.res);
     std::vector<u32> base(kParts + 1);
     if ((e = cudaMemcpyAsync(base.data(), c.base, (kParts + 1) * 4, cudaMemcpyDeviceToHost, st)) !=
