@@ -181,7 +181,10 @@ rg_status rg_route_pairs(rg_ctx* ctx, const uint64_t* keys, const uint64_t* coun
 /* Adds (packed key, count) pairs produced by rg_export_entries of an
  * accumulator with equal params: the counts-add half of
  * TileAccumulator::merge (accumulator.hpp:137-154) for pairs that arrive
- * over the network. total_ingested grows by the summed counts. */
+ * over the network. total_ingested grows by the summed counts. Keys are
+ * checked first: a key that is not a packed key of this context (all ones,
+ * or bits above the column and row fields) fails the call with RG_ERR_ARG
+ * and nothing is added. */
 rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts,
                            uint64_t n, rg_memkind kind);
 

@@ -118,6 +118,20 @@ __global__ void k_fingerprint(const double* xy, u64 n, u64* out) {
     if (lane == 0) *out = h;
 }
 
+// Packed keys handed in by a caller (rg_ingest_counts): every key must be a
+// key of this context's packing (not the EMPTY word, no bits above the
+// column and row fields). Counts the offenders.
+__global__ void k_check_keys(const u64* keys, u64 n, u32 key_bits, u64* bad) {
+    u32 b = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 k = keys[i];
+        b += (k == kEmpty || (key_bits < 64 && (k >> key_bits) != 0)) ? 1u : 0u;
+    }
+    b = __reduce_add_sync(kFull, b);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, (u64)b);
+}
+
 __global__ void k_iota(u32* out, u64 n) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x)
@@ -1935,7 +1949,26 @@ rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* co
         dk = tk;
         dc = tc;
     }
-    CK(cudaMemsetAsync(ctx->scratch, 0, 2 * sizeof(u64), ctx->st));
+    // keys must come from rg_export_entries / rg_route_pairs of a context with
+    // the same parameters: anything else would alias the table's EMPTY word
+    CK(cudaMemsetAsync(ctx->scratch, 0, 3 * sizeof(u64), ctx->st));
+    {
+        const u64 want = (n + 255) / 256;
+        k_check_keys<<<(int)std::max<u64>(1, std::min<u64>(want, (u64)ctx->n_sm * 8)), 256, 0,
+                       ctx->st>>>(dk, n, ctx->res.bits_x + ctx->res.bits_y, ctx->scratch + 2);
+        ++ctx->launches;
+        u64 bad = 0;
+        CK(cudaMemcpyAsync(&bad, ctx->scratch + 2, sizeof bad, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (bad) {
+            dfree(tk);
+            dfree(tc);
+            return set_err(ctx, RG_ERR_ARG,
+                           "%llu of %llu keys are not packed keys of this context (use "
+                           "rg_export_entries of a context with the same parameters)",
+                           (unsigned long long)bad, (unsigned long long)n);
+        }
+    }
     CK(launch_pairs_fold(dk, dc, n, table_of(ctx), ctx->scratch, ctx->scratch + 1, ctx->n_sm,
                          ctx->st));
     ++ctx->launches;

@@ -187,9 +187,19 @@ def _all_to_all(dist, group, send, send_counts, torch):
     rc = torch.empty(world, dtype=torch.int64, device=wire)
     dist.all_to_all_single(rc, sc, group=group)
     recv_counts = rc.cpu().tolist()
-    out = torch.empty(int(sum(recv_counts)), dtype=send.dtype, device=wire)
+    out = torch.empty((int(sum(recv_counts)),) + tuple(send.shape[1:]), dtype=send.dtype,
+                      device=wire)
     dist.all_to_all_single(out, send, recv_counts, list(send_counts), group=group)
     return out.to(home), recv_counts
+
+
+def _all_to_all_pairs(dist, group, keys, cnts, send_counts, torch):
+    """(key, count) pairs to their owners in ONE exchange of a [m, 2] int64
+    tensor (rows split by destination), instead of one per column."""
+    kd, cd = keys.dtype, cnts.dtype
+    pairs = torch.stack([keys.view(torch.int64), cnts.view(torch.int64)], 1).contiguous()
+    out, _ = _all_to_all(dist, group, pairs, send_counts, torch)
+    return out[:, 0].contiguous().view(kd), out[:, 1].contiguous().view(cd)
 
 
 def _all_gather_var(dist, group, t, torch):
@@ -310,8 +320,7 @@ class DistributedPipeline:
                 order = torch.argsort(owner, stable=True)
                 keys, cnts = keys[order], cnts[order]
                 send_counts = torch.bincount(owner, minlength=world).cpu().tolist()
-            keys, _ = _all_to_all(dist, group, keys, send_counts, torch)
-            cnts, _ = _all_to_all(dist, group, cnts, send_counts, torch)
+            keys, cnts = _all_to_all_pairs(dist, group, keys, cnts, send_counts, torch)
             st.bytes_sent = 16 * st.n_local_entries
         st.n_owned = int(keys.numel())
         tx, ty, cnt, cid, size = eng.owner_cluster(keys, cnts)

@@ -70,6 +70,16 @@ def test_export_host_and_ingest_counts_host():
     assert b.entry_count() == d and b.total_ingested() == 2 * len(pts)
     ca, cb = a.counts(), b.counts()
     assert ca.keys() == cb.keys() and all(cb[t] == 2 * ca[t] for t in ca)
+    # keys that are not packed keys of this context are rejected before any
+    # of them reaches the table (EMPTY would alias free slots)
+    before = b.counts()
+    for badkey in (np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64(1) << np.uint64(62)):
+        bk = keys.copy()
+        bk[d // 2] = badkey
+        with pytest.raises(Exception, match="not packed keys"):
+            b._ctx.check(b._ctx.lib.rg_ingest_counts(b._ctx.h, bk.ctypes.data, cnts.ctypes.data,
+                                                     d, N.RG_MEM_HOST))
+    assert b.counts() == before and b.total_ingested() == 2 * len(pts)
     # a too-small export buffer is an argument error, not a partial write
     with pytest.raises(Exception):
         ctx.check(ctx.lib.rg_export_entries(ctx.h, keys.ctypes.data, cnts.ctypes.data, d - 1,
