@@ -16,6 +16,8 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+
+import numpy as np
 import json
 import os
 import statistics
@@ -221,6 +223,39 @@ def cpu_baseline_sequential(pts_host, gp, n_count: int, n_retain: int) -> dict:
             "sample": f"first {n_retain:,} points, raster::cluster_sequential Mode::retain_points, "
                       "1 thread, 1 run (the reference's point-retaining variant)"}
     return out
+
+
+def stream_leg(gp, pts) -> dict:
+    """The chunked PointSource path (rg_stream_*, io.hpp:226-241): a
+    memory-backed source whose read() copies the next chunk into the pinned
+    staging buffer, while the previous chunk's H2D copy and K1 run. Host
+    wall clock from the first read to the last chunk's contraction (the
+    source's copies are part of the job, as a file read would be)."""
+    from paper_1907_03620_b200.raster import TileAccumulator
+
+    chunk = 1 << 22
+    acc = TileAccumulator(gp)
+    pos = [0]
+
+    def read(out):
+        k = min(len(out), len(pts) - pos[0])
+        np.copyto(out[:k], pts[pos[0]:pos[0] + k])
+        pos[0] += k
+        return k
+
+    acc.ingest_source(read, chunk)  # warm-up (buffers, table)
+    del acc
+    pos[0] = 0
+    acc2 = TileAccumulator(gp)
+    acc2.ingest_source(lambda out: 0, chunk)
+    t0 = time.perf_counter()
+    n = acc2.ingest_source(read, chunk)
+    t = time.perf_counter() - t0
+    assert acc2.total_ingested() + acc2.skipped() == len(pts)
+    return {"points_per_s": n / t, "seconds": t, "chunk_points": chunk,
+            "source": "memory-backed PointSource: read() = numpy copy of the next chunk into the "
+                      "pinned buffer (single host thread), overlapped with the previous chunk's "
+                      "H2D + K1"}
 
 
 def per_config_sweep(args, pl4, stream, dev4) -> dict:
@@ -445,6 +480,7 @@ def ours(args) -> None:
         del shuf
 
     if not args.quick and world == 1:
+        extra["stream"] = stream_leg(gp, host.numpy())
         extra["per_config"] = per_config_sweep(args, pl, stream, dev if cfg == 4 else None)
 
     peak, peak_src = measured_peak_gbs()

@@ -255,7 +255,8 @@ inline ClusterSet agglomerate(SignificantTiles sig, const GridParams& params) {
 }
 
 /// cluster_sequential pipeline.hpp:92-126 over a PointSource (single pass:
-/// the whole-span fast path io.hpp:50-54 or 1 Mi-point chunks).
+/// the whole-span fast path io.hpp:50-54, or 4 Mi-point chunks read into
+/// pinned buffers while the previous chunk is copied and contracted).
 inline ClusterSet cluster_sequential(PointSource& src, const GridParams& params,
                                      bool use_window_fix = false, PipelineStats* stats = nullptr) {
     params.validate();
@@ -268,13 +269,25 @@ inline ClusterSet cluster_sequential(PointSource& src, const GridParams& params,
         acc.ingest(*span);
         all = *span;
     } else {
-        std::vector<Point> buf(std::size_t{1} << 20);
+        // chunked source: the next read fills one pinned buffer while the
+        // previous chunk is copied and contracted (rg_stream_*)
+        rg_ctx* sctx = acc.handle();
+        check(rg_stream_begin(sctx, std::uint64_t{1} << 22), sctx);
         while (true) {
-            const std::size_t n = src.read(buf);
+            double* buf = nullptr;
+            std::uint64_t cap = 0;
+            check(rg_stream_buffer(sctx, &buf, &cap), sctx);
+            std::span<Point> out(reinterpret_cast<Point*>(buf), static_cast<std::size_t>(cap));
+            const std::size_t n = src.read(out);
             if (n == 0) break;
-            acc.ingest(std::span<const Point>(buf.data(), n));
-            if (params.mode == Mode::retain_points) kept.insert(kept.end(), buf.begin(), buf.begin() + n);
+            if (params.mode == Mode::retain_points) kept.insert(kept.end(), out.begin(), out.begin() + n);
+            const rg_status s = rg_stream_submit(sctx, n);
+            if (s != RG_OK) {
+                rg_stream_end(sctx);
+                check(s, sctx);
+            }
         }
+        check(rg_stream_end(sctx), sctx);
         all = kept;
     }
     rg_ctx* ctx = acc.handle();

@@ -146,6 +146,23 @@ rg_status rg_reset(rg_ctx* ctx);
  * ingested, none after it (as the reference's throwing loop). */
 rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind);
 
+/* Streaming ingest: what ingest_all (io.hpp:226-241) does with a chunked
+ * PointSource (io.hpp:21-36), with the source's next read overlapped with
+ * the previous chunk's host-to-device copy and contraction.
+ *   rg_stream_begin(ctx, chunk)   two pinned host buffers of `chunk` points
+ *                                 (0: 4 Mi points)
+ *   rg_stream_buffer(ctx, &buf, &cap)  the next buffer to fill (waits until
+ *                                 its previous copy has left it)
+ *   rg_stream_submit(ctx, n)      ingest its first n points; returns at once
+ *   rg_stream_end(ctx)            waits for every chunk; counters are final
+ * The accumulator semantics are those of rg_ingest on each chunk in order
+ * (strict policy: the first out-of-bounds point ends the stream with
+ * RG_ERR_OOB after the points before it). */
+rg_status rg_stream_begin(rg_ctx* ctx, uint64_t chunk_points);
+rg_status rg_stream_buffer(rg_ctx* ctx, double** buf, uint64_t* capacity);
+rg_status rg_stream_submit(rg_ctx* ctx, uint64_t n);
+rg_status rg_stream_end(rg_ctx* ctx);
+
 /* TileAccumulator::merge accumulator.hpp:137-154: folds src into dst (counts
  * add); src is left empty. Both must have equal params. */
 rg_status rg_merge(rg_ctx* dst, rg_ctx* src);

@@ -110,6 +110,10 @@ GPU_SYMBOLS = {
     "rg_synchronize": (ST, [P]),
     "rg_reset": (ST, [P]),
     "rg_ingest": (ST, [P, P, U64, ST]),
+    "rg_stream_begin": (ST, [P, U64]),
+    "rg_stream_buffer": (ST, [P, P, P]),
+    "rg_stream_submit": (ST, [P, U64]),
+    "rg_stream_end": (ST, [P]),
     "rg_merge": (ST, [P, P]),
     "rg_clone": (ST, [P, C.POINTER(P)]),
     "rg_key_packing": (ST, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(C.c_uint32)]),

@@ -386,6 +386,13 @@ struct rg_ctx {
     double* stage[2] = {nullptr, nullptr};
     int* lstage[2] = {nullptr, nullptr};
     u64 stage_pts = 0;
+    // streaming ingest (rg_stream_*): pinned host buffers the source fills
+    double* pin[2] = {nullptr, nullptr};
+    cudaEvent_t pin_free[2] = {nullptr, nullptr};  // its H2D copy has finished
+    u64 pin_pts = 0;
+    int pin_next = 0, pin_held = -1;
+    u64 stream_chunks = 0;
+    bool streaming = false;
 
     double ms_contract = 0, ms_prune = 0, ms_agg = 0, ms_label = 0;
     u64 launches = 0;
@@ -1686,6 +1693,10 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->pair_cnt);
     dfree(ctx->lk_tab);
     dfree(ctx->lk_ids);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+        if (ctx->pin_free[b]) cudaEventDestroy(ctx->pin_free[b]);
+    }
     dfree(ctx->sort_temp);
     dfree(ctx->offsets);
     for (int b = 0; b < 2; ++b) {
@@ -1721,11 +1732,126 @@ rg_status rg_synchronize(rg_ctx* ctx) {
     return RG_OK;
 }
 
+static rg_status settle_stream(rg_ctx* ctx);
+
 rg_status rg_ingest(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
     DevGuard guard(ctx->device);
     return ingest_any(ctx, xy, n, kind);
+}
+
+// ------------------------------------------------------ streaming ingest
+// PointSource reads (io.hpp:21-36) drained chunk by chunk (ingest_all
+// io.hpp:226-241) with the source's next read overlapped with the current
+// chunk's H2D copy and K1: the context hands out one of two pinned host
+// buffers, the caller fills it, rg_stream_submit enqueues the copy (copy
+// stream) and K1 (compute stream) and returns; K1's stop check of a chunk
+// runs when the next chunk is submitted (or at rg_stream_end).
+rg_status rg_stream_begin(rg_ctx* ctx, uint64_t chunk_points) {
+    if (!ctx) return RG_ERR_ARG;
+    if (ctx->streaming) return set_err(ctx, RG_ERR_STATE, "a stream is already open");
+    DevGuard guard(ctx->device);
+    rg_status s = reopen_accumulator(ctx);
+    if (s != RG_OK) return s;
+    const u64 want = std::max<u64>(1024, std::min<u64>(chunk_points ? chunk_points : (1ull << 22),
+                                                       kStagePoints));
+    if (ctx->pin_pts < want) {
+        for (int b = 0; b < 2; ++b) {
+            if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+            ctx->pin[b] = nullptr;
+        }
+        ctx->pin_pts = 0;
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMallocHost((void**)&ctx->pin[b], want * 2 * sizeof(double)));
+            if (!ctx->pin_free[b]) CK(cudaEventCreateWithFlags(&ctx->pin_free[b],
+                                                               cudaEventDisableTiming));
+        }
+        ctx->pin_pts = want;
+    }
+    s = ensure_stage(ctx, ctx->pin_pts, false);
+    if (s != RG_OK) return s;
+    ctx->pin_next = 0;
+    ctx->pin_held = -1;
+    ctx->stream_chunks = 0;
+    ctx->chunk_verdict = -1;
+    ctx->streaming = true;
+    return RG_OK;
+}
+
+rg_status rg_stream_buffer(rg_ctx* ctx, double** buf, uint64_t* capacity) {
+    if (!ctx || !buf || !capacity) return RG_ERR_ARG;
+    if (!ctx->streaming) return set_err(ctx, RG_ERR_STATE, "rg_stream_begin first");
+    DevGuard guard(ctx->device);
+    const int b = ctx->pin_next;
+    CK(cudaEventSynchronize(ctx->pin_free[b]));  // (never recorded: complete)
+    ctx->pin_held = b;
+    *buf = ctx->pin[b];
+    *capacity = ctx->pin_pts;
+    return RG_OK;
+}
+
+rg_status rg_stream_submit(rg_ctx* ctx, uint64_t n) {
+    if (!ctx) return RG_ERR_ARG;
+    if (!ctx->streaming || ctx->pin_held < 0)
+        return set_err(ctx, RG_ERR_STATE, "rg_stream_buffer first");
+    if (n > ctx->pin_pts) return set_err(ctx, RG_ERR_ARG, "more points than the buffer holds");
+    DevGuard guard(ctx->device);
+    const int b = ctx->pin_held;
+    ctx->pin_held = -1;
+    ctx->pin_next = 1 - b;
+    if (n == 0) return RG_OK;
+    if (ctx->k1.active) {  // the previous chunk's stop check (it has usually finished)
+        rg_status s = k1_finish(ctx);
+        if (s != RG_OK) return s;
+    }
+    CK(cudaStreamWaitEvent(ctx->copy_st, ctx->done[b], 0));  // device staging b is free
+    CK(cudaMemcpyAsync(ctx->stage[b], ctx->pin[b], n * 2 * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->copy_st));
+    CK(cudaEventRecord(ctx->pin_free[b], ctx->copy_st));
+    CK(cudaEventRecord(ctx->copied[b], ctx->copy_st));
+    CK(cudaStreamWaitEvent(ctx->st, ctx->copied[b], 0));
+    bool oob = false;
+    double ox = 0, oy = 0;
+    rg_status s = ingest_span(ctx, ctx->stage[b], n, &oob, &ox, &oy,
+                              ctx->p.oob_policy != RG_OOB_STRICT);
+    if (s != RG_OK) return s;
+    CK(cudaEventRecord(ctx->done[b], ctx->st));
+    // the first chunk's order verdict holds for the rest of the stream
+    if (ctx->stream_chunks++ == 0 && ctx->probe_ptr == ctx->stage[b])
+        ctx->chunk_verdict = ctx->probe_unordered;
+    if (oob) {
+        ctx->streaming = false;
+        ctx->chunk_verdict = -1;
+        CK(cudaStreamSynchronize(ctx->copy_st));
+        return oob_error(ctx, ox, oy);
+    }
+    return RG_OK;
+}
+
+rg_status rg_stream_end(rg_ctx* ctx) {
+    if (!ctx) return RG_ERR_ARG;
+    if (!ctx->streaming) return RG_OK;
+    DevGuard guard(ctx->device);
+    ctx->streaming = false;
+    ctx->chunk_verdict = -1;
+    if (ctx->k1.active) {
+        rg_status s = k1_finish(ctx);
+        if (s != RG_OK) return s;
+    }
+    CK(cudaStreamSynchronize(ctx->copy_st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return RG_OK;
+}
+
+// Any other call on a context with an open stream closes it first (its
+// counters and table must be final).
+static rg_status settle_stream(rg_ctx* ctx) {
+    return ctx->streaming ? rg_stream_end(ctx) : RG_OK;
 }
 
 static rg_status clone_into(rg_ctx* ctx, rg_ctx* src) {
@@ -1758,6 +1884,10 @@ static rg_status clone_into(rg_ctx* ctx, rg_ctx* src) {
 
 rg_status rg_clone(rg_ctx* src, rg_ctx** out) {
     if (!src || !out) return set_err(nullptr, RG_ERR_ARG, "null argument");
+    if (src) {
+        const rg_status ss = settle_stream(src);
+        if (ss != RG_OK) return ss;
+    }
     *out = nullptr;
     rg_ctx* dst = nullptr;
     rg_status s = rg_create(&src->p, src->device, &dst);
@@ -1774,6 +1904,10 @@ rg_status rg_clone(rg_ctx* src, rg_ctx** out) {
 }
 
 rg_status rg_merge(rg_ctx* dst, rg_ctx* src) {
+    if (dst) {
+        const rg_status ss = settle_stream(dst);
+        if (ss != RG_OK) return ss;
+    }
     rg_ctx* ctx = dst;
     if (!dst || !src) return RG_ERR_ARG;
     if (dst == src) return set_err(dst, RG_ERR_ARG, "cannot merge an accumulator into itself");
@@ -1862,6 +1996,10 @@ rg_status rg_key_packing(rg_ctx* ctx, int64_t* origin_x, int64_t* origin_y, uint
 rg_status rg_export_entries(rg_ctx* ctx, uint64_t* keys, uint64_t* counts, uint64_t cap,
                             uint64_t* n_out, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     const u64 d = (ctx->state == rg_ctx::kAccum && ctx->slots) ? ctx->used : 0;
     if (n_out) *n_out = d;
     if (d == 0 || cap == 0) return RG_OK;
@@ -1926,6 +2064,10 @@ rg_status rg_route_pairs(rg_ctx* ctx, const uint64_t* keys, const uint64_t* coun
 rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* counts,
                            uint64_t n, rg_memkind kind) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (dedupe_active(ctx))
         return set_err(ctx, RG_ERR_UNSUPPORTED,
                        "count pairs cannot be deduplicated (dedupe_points needs the points)");
@@ -1984,24 +2126,40 @@ rg_status rg_ingest_counts(rg_ctx* ctx, const uint64_t* keys, const uint64_t* co
 
 rg_status rg_entry_count(rg_ctx* ctx, uint64_t* out) {
     if (!ctx || !out) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     *out = ctx->state == rg_ctx::kAccum ? ctx->used : 0;
     return RG_OK;
 }
 
 rg_status rg_total_ingested(rg_ctx* ctx, uint64_t* out) {
     if (!ctx || !out) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     *out = ctx->ingested;
     return RG_OK;
 }
 
 rg_status rg_skipped(rg_ctx* ctx, uint64_t* out) {
     if (!ctx || !out) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     *out = ctx->skipped;
     return RG_OK;
 }
 
 rg_status rg_count_of(rg_ctx* ctx, int64_t tx, int64_t ty, uint64_t* out) {
     if (!ctx || !out) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     *out = 0;
     if (ctx->state != rg_ctx::kAccum || !ctx->slots || ctx->used == 0) return RG_OK;
     const Grid& g = ctx->grid;
@@ -2022,6 +2180,10 @@ rg_status rg_count_of(rg_ctx* ctx, int64_t tx, int64_t ty, uint64_t* out) {
 rg_status rg_export_counts(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* count, uint64_t cap,
                            uint64_t* n_out) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (ctx->state != rg_ctx::kAccum || !ctx->slots || ctx->used == 0) {
         if (n_out) *n_out = 0;
         return RG_OK;
@@ -2050,6 +2212,10 @@ rg_status rg_export_counts(rg_ctx* ctx, int64_t* tx, int64_t* ty, uint64_t* coun
 
 rg_status rg_prune(rg_ctx* ctx, uint64_t* n_significant) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     DevGuard guard(ctx->device);
     rg_status s = prune_impl(ctx);
     if (s == RG_OK && n_significant) *n_significant = ctx->n_sig;
@@ -2058,6 +2224,10 @@ rg_status rg_prune(rg_ctx* ctx, uint64_t* n_significant) {
 
 rg_status rg_window_fix(rg_ctx* ctx, uint64_t* n_significant) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     DevGuard guard(ctx->device);
     rg_status s = prune_impl(ctx, true);
     if (s == RG_OK && n_significant) *n_significant = ctx->n_sig;
@@ -2182,6 +2352,10 @@ rg_status rg_agglomerate(rg_ctx* ctx, uint64_t* n_clusters) {
 }
 
 rg_status rg_get_stats(rg_ctx* ctx, rg_stats* out) {
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (ctx) resolve_contract_timer(ctx);
     if (!ctx || !out) return RG_ERR_ARG;
     std::memset(out, 0, sizeof *out);
@@ -2269,6 +2443,10 @@ static rg_status reset_impl(rg_ctx* ctx) {
 
 rg_status rg_reset(rg_ctx* ctx) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     DevGuard guard(ctx->device);
     return reset_impl(ctx);
 }
@@ -2281,6 +2459,10 @@ rg_status rg_cluster(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
 rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind kind,
                         uint32_t flags, rg_stats* stats) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (flags & ~(uint32_t)RG_CLUSTER_WINDOW_FIX)
         return set_err(ctx, RG_ERR_ARG, "unknown rg_cluster_ex flags 0x%x", flags);
     if (n && !xy) return set_err(ctx, RG_ERR_ARG, "null point buffer");
@@ -2312,6 +2494,10 @@ rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind ki
 
 rg_status rg_prune_agglomerate(rg_ctx* ctx, uint32_t flags, rg_stats* stats) {
     if (!ctx) return RG_ERR_ARG;
+    if (ctx) {
+        const rg_status ss = settle_stream(ctx);
+        if (ss != RG_OK) return ss;
+    }
     if (flags & ~(uint32_t)RG_CLUSTER_WINDOW_FIX)
         return set_err(ctx, RG_ERR_ARG, "unknown rg_prune_agglomerate flags 0x%x", flags);
     DevGuard guard(ctx->device);

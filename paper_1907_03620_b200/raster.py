@@ -339,6 +339,29 @@ class TileAccumulator:
         p = _Points(pts, getattr(self, "_settle", True))
         self._ctx.check(self._ctx.lib.rg_ingest(self._ctx.h, p.ptr, p.n, p.kind))
 
+    def ingest_source(self, read, chunk_points: int = 1 << 22) -> int:
+        """ingest_all io.hpp:226-241 over a PointSource-like callable:
+        read(out) fills the (k, 2) float64 array `out` (a pinned staging
+        buffer) with up to k points and returns how many it wrote (0: the
+        source is exhausted). Each chunk's copy and contraction run while the
+        next read fills the other buffer. Returns the points read."""
+        lib, h = self._ctx.lib, self._ctx.h
+        self._ctx.check(lib.rg_stream_begin(h, int(chunk_points)))
+        total = 0
+        try:
+            while True:
+                buf, cap = C.c_void_p(), C.c_uint64()
+                self._ctx.check(lib.rg_stream_buffer(h, C.byref(buf), C.byref(cap)))
+                out = np.ctypeslib.as_array((C.c_double * (2 * cap.value)).from_address(buf.value))
+                k = int(read(out.reshape(-1, 2)))
+                if k <= 0:
+                    break
+                self._ctx.check(lib.rg_stream_submit(h, k))
+                total += k
+        finally:
+            self._ctx.check(lib.rg_stream_end(h))
+        return total
+
     def merge(self, other: "TileAccumulator") -> None:
         """accumulator.hpp:137-154"""
         self._ctx.check(self._ctx.lib.rg_merge(self._ctx.h, other._ctx.h))

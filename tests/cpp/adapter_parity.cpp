@@ -188,7 +188,8 @@ int main() {
             std::size_t read(std::span<Point> out) override { return src.read(out); }
             VectorSource src;
         };
-        const auto pts = gaussian_clusters(300, 4000, 0.0005, 4242, 0.05);  // > 1 Mi points
+        // > 4 Mi points: the stream-only source takes two pinned 4 Mi-point chunks
+        const auto pts = gaussian_clusters(1100, 4000, 0.0005, 4242, 0.05);
         for (int prime = 0; prime < 2; ++prime) {
             GridParams params;
             params.precision = 3.0;

@@ -332,3 +332,35 @@ def test_stream_ordering_with_torch_default_stream():
         dst.copy_(src.flip(0))  # still running when the next call is enqueued
         pl.run(dst)
         assert_same(pl.flat(), want)
+
+
+@pytest.mark.parametrize("chunk", [65536, 1 << 20])
+def test_streaming_ingest_matches_single_span(chunk):
+    """rg_stream_* (a PointSource drained chunk by chunk with the next read
+    overlapping the previous chunk's copy and K1, io.hpp:226-241): counts,
+    counters and table identical to one rg_ingest of the whole span, for
+    ordered and shuffled sources; strict policy stops at the first
+    out-of-bounds point."""
+    import numpy as np
+
+    from paper_1907_03620_b200 import datagen as D
+    from paper_1907_03620_b200.raster import TileAccumulator
+
+    gp = D.params(3)
+    for shuffle in (None, 3):
+        pts = D.generate(D.spec(3, 0.05), shuffle_seed=shuffle)
+        pts[::7919] = [1000.0, 0.0]
+        one = TileAccumulator(gp)
+        one.ingest(pts)
+        st = TileAccumulator(gp)
+        pos = [0]
+
+        def read(out):
+            k = min(len(out), len(pts) - pos[0])
+            out[:k] = pts[pos[0]:pos[0] + k]
+            pos[0] += k
+            return k
+
+        assert st.ingest_source(read, chunk) == len(pts)
+        assert st.counts() == one.counts()
+        assert (st.total_ingested(), st.skipped()) == (one.total_ingested(), one.skipped())
