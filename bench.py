@@ -51,9 +51,10 @@ def measured_peak_gbs() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled through NVML every ~2 ms while
+    """SM clocks + throttle reasons sampled through NVML every ~5 ms while
     the timed region runs (the recipe's nvidia-smi clocks line, at a rate
-    that also covers short regions)."""
+    that also covers short regions; a 2 ms period measurably slowed the
+    launch thread through the GIL)."""
 
     REASONS = {
         "hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
@@ -63,7 +64,7 @@ class ClockSampler:
         "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown",
     }
 
-    def __init__(self, index: int, period_s: float = 0.002):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
         self.period = period_s
         self.sm: list[float] = []
@@ -108,7 +109,7 @@ class ClockSampler:
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "NVML, 2 ms period, timed region only"}
+                "samples": len(self.sm), "source": "NVML, 5 ms period, timed region only"}
 
 
 def k1_traffic(n: int):
