@@ -710,7 +710,11 @@ __global__ void k_first_oob(const double* xy, u64 n, Grid g, u64* first) {
 #define RG_K2_ITEMS 4
 #endif
 constexpr int kK2Items = RG_K2_ITEMS;
-constexpr int kK2Stage = 256 + 32 * kK2Items;
+#ifndef RG_K2_FLUSH
+#define RG_K2_FLUSH 128
+#endif
+constexpr u32 kK2Flush = RG_K2_FLUSH;  // staged entries that trigger a write-out
+constexpr int kK2Stage = kK2Flush + 32 * kK2Items;
 
 struct K2Out {
     u64* sig_key;
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, cons
             if (k[j] != kEmpty && v[j] >= tau) s_idx[p++] = (u32)(base + j * 32 + lane);
         slen += total;
         __syncwarp();
-        if (slen >= 256) {
+        if (slen >= kK2Flush) {
             k2_flush(t, s_idx, slen, out, ctr, lane);
             slen = 0;
         }

@@ -168,6 +168,9 @@ __device__ __forceinline__ u32 cell_bit(u64 key, u32 bits_y) {
 // flagged mixed. *n_cells counts cells; *over flags a table that filled up.
 __global__ void k_cells_build(const u64* skey, const int* cid, const u64* n_p, ulonglong2* tab,
                               u64 nb, u32 bits_y, u64 cap_cells, u64* n_cells, u32* over) {
+    __shared__ u32 s_new;
+    if (threadIdx.x == 0) s_new = 0;
+    __syncthreads();
     const u64 n = *n_p;
     const int lane = threadIdx.x & 31;
     const u64 span = (n + 31) / 32 * 32;  // whole warps: the aggregation below is warp-wide
@@ -212,10 +215,12 @@ __global__ void k_cells_build(const u64* skey, const int* cid, const u64* n_p, u
         else
             *over = 1;
         }
-        // new cells counted once per warp (one counter would serialise)
+        // new cells counted per block (one global counter would serialise)
         const u32 nf = __popc(__ballot_sync(kFull, fresh));
-        if (lane == 0 && nf && atomicAdd(n_cells, (u64)nf) + nf > cap_cells) *over = 1;
+        if (lane == 0 && nf) atomicAdd(&s_new, nf);
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_new && atomicAdd(n_cells, (u64)s_new) + s_new > cap_cells) *over = 1;
 }
 
 // Pass 2: mixed cells get a base in the per-tile id array.
