@@ -114,9 +114,9 @@ class ClockSampler:
 
 def k1_traffic(n: int):
     """dram bytes per K1 launch from the committed ncu --set full capture
-    (profiles/r01/k1_traffic.json), scaled to this workload; None if absent."""
+    (profiles/r02/k1_traffic.json), scaled to this workload; None if absent."""
     try:
-        d = json.loads((ROOT / "profiles" / "r01" / "k1_traffic.json").read_text())
+        d = json.loads((ROOT / "profiles" / "r02" / "k1_traffic.json").read_text())
         return d["traffic_bytes_per_launch"] * n / (d["algorithmic_bytes_per_launch"] / BYTES_PER_POINT)
     except Exception:
         return None
@@ -501,7 +501,7 @@ def ours(args) -> None:
                    "border join of the range edges (small all_gathers)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": k1_traffic(n) if cfg == 4 else None,
-                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01)",
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r02)",
                      "kernel": "K1 contraction (k_contract), 16 B/point, ms from CUDA events on the launch stream",
                      "peak_source": peak_src,
                      "end_to_end_frac": (BYTES_PER_POINT * n / (ms_step / 1e3) / 1e9) / peak},
