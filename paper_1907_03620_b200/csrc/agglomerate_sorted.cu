@@ -457,80 +457,7 @@ __global__ void k_sorted_reduce(u32* parent, const u32* perm, const u64* cnt_b,
 
 
 // ---------------------------------------------------- single-pass scans
-// Decoupled look-back (one pass, no library scan): a block takes the next
-// tile from a ticket, publishes its aggregate, reads its predecessors'
-// published values back to the first inclusive prefix, and publishes its
-// own inclusive prefix. Status word: flag (2 bits) << 62 | value.
-constexpr u64 kLbAgg = 1ull << 62, kLbPre = 2ull << 62, kLbVal = (1ull << 62) - 1;
-
-__device__ __forceinline__ void lb_store(u64* p, u64 v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ u64 lb_load(const u64* p) {
-    u64 v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Called by one whole warp: the exclusive prefix of `tile` given its
-// aggregate. The warp inspects 32 predecessors at a time (each lane waits
-// until its predecessor has published something), adds up aggregates back to
-// the nearest inclusive prefix, and publishes its own inclusive prefix.
-__device__ __forceinline__ u64 lb_prefix(u64* status, u32 tile, u64 agg) {
-    const int lane = threadIdx.x & 31;
-    if (tile == 0) {
-        if (lane == 0) lb_store(status, kLbPre | agg);
-        return 0;
-    }
-    if (lane == 0) lb_store(status + tile, kLbAgg | agg);
-    u64 pre = 0;
-    for (long long j = (long long)tile - 1;; j -= 32) {
-        const long long idx = j - lane;
-        u64 v = kLbPre;  // before tile 0: an inclusive prefix of 0
-        if (idx >= 0)
-            while (((v = lb_load(status + idx)) >> 62) == 0) {
-            }
-        const u32 pm = __ballot_sync(kFull, (v >> 62) == 2);
-        // lanes up to the nearest inclusive prefix (all 32 when none)
-        const int last = pm ? __ffs(pm) - 1 : 31;
-        u64 x = lane <= last ? (v & kLbVal) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-        pre += x;
-        if (pm) break;
-    }
-    if (lane == 0) lb_store(status + tile, kLbPre | (pre + agg));
-    return pre;
-}
-
-// Block-wide exclusive sum of one u32 per thread (kThr threads); the block
-// total through *total.
-template <int kThr>
-__device__ __forceinline__ u32 block_excl_sum(u32 v, u32* s_warp, u32* total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u32 incl = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const u32 y = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += y;
-    }
-    if (lane == 31) s_warp[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        const u32 w = lane < kThr / 32 ? s_warp[lane] : 0;
-        u32 wi = w;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const u32 y = __shfl_up_sync(kFull, wi, d);
-            if (lane >= d) wi += y;
-        }
-        if (lane < kThr / 32) s_warp[lane] = wi - w;
-        if (lane == 31) s_warp[32] = wi;
-    }
-    __syncthreads();
-    *total = s_warp[32];
-    return s_warp[wid] + incl - v;
-}
+// (decoupled look-back helpers: common.cuh)
 
 // Column offsets for the column-ordered K3 in one pass (replaces a column
 // maximum pass, a library scan and a bucket-bounds search): col_off =
@@ -828,9 +755,21 @@ __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 
             }
         }
         __syncthreads();
-        for (u32 b = threadIdx.x; b < nbkt; b += kP1Threads) {
-            const u32 c = hist[b];
-            if (c) base[b] = atomicAdd(cur + b, c);
+        // one reservation per (tile, bucket); a thread's reservations are
+        // issued together (their round trips overlap instead of queueing)
+        for (u32 b0 = threadIdx.x; b0 < nbkt; b0 += 4 * kP1Threads) {
+            u32 r[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u32 b = b0 + q * kP1Threads;
+                const u32 c = b < nbkt ? hist[b] : 0;
+                r[q] = c ? atomicAdd(cur + b, c) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u32 b = b0 + q * kP1Threads;
+                if (b < nbkt) base[b] = r[q];
+            }
         }
         __syncthreads();
 #pragma unroll

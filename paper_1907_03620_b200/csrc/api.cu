@@ -366,6 +366,8 @@ struct rg_ctx {
     u64 pair_cap = 0;
     u64 order_probe[3] = {0, 0, 0};
     u64 probe_fp = 0;       // fingerprint of the probed buffer's content
+    u64* k2_lb = nullptr;   // K2's look-back status words
+    u64 k2_lb_words = 0;
     // K4' cell table of the kept tiles (labels of unordered inputs)
     ulonglong2* lk_tab = nullptr;
     int* lk_ids = nullptr;
@@ -1242,11 +1244,18 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
             if (s != RG_OK) return s;
             CK(cudaMemsetAsync(ctx->s_col_cnt, 0, (cols + 1) * sizeof(u32), ctx->st));
         }
+        if (ctx->k2_lb_words < compact_lb_words(ctx->cap)) {
+            dfree(ctx->k2_lb);
+            ctx->k2_lb_words = 0;
+            CK(dalloc(&ctx->k2_lb, compact_lb_words(ctx->cap)));
+            ctx->k2_lb_words = compact_lb_words(ctx->cap);
+        }
         CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
                           window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
                           ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
                           ctx->root_cid, cols ? ctx->s_col_cnt : nullptr,
-                          hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st));
+                          hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st,
+                          ctx->k2_lb));
         ++ctx->launches;
         ctx->col_hist_ready = cols != 0;
         if (ctx->alt_dirty && ctx->slots_alt && ctx->cap_alt == ctx->cap) {
@@ -1693,6 +1702,7 @@ void rg_destroy(rg_ctx* ctx) {
     dfree(ctx->pair_cnt);
     dfree(ctx->lk_tab);
     dfree(ctx->lk_ids);
+    dfree(ctx->k2_lb);
     for (int b = 0; b < 2; ++b) {
         if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
         if (ctx->pin_free[b]) cudaEventDestroy(ctx->pin_free[b]);

@@ -319,4 +319,82 @@ struct Partial {
     u64 next_row;
 };
 
+// ---------------------------------------------------- single-pass scans (K2, K3)
+// Decoupled look-back (one pass, no library scan): a block takes the next
+// tile from a ticket, publishes its aggregate, reads its predecessors'
+// published values back to the first inclusive prefix, and publishes its
+// own inclusive prefix. Status word: flag (2 bits) << 62 | value.
+constexpr u64 kLbAgg = 1ull << 62, kLbPre = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_store(u64* p, u64 v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 lb_load(const u64* p) {
+    u64 v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Called by one whole warp: the exclusive prefix of `tile` given its
+// aggregate. The warp inspects 32 predecessors at a time (each lane waits
+// until its predecessor has published something), adds up aggregates back to
+// the nearest inclusive prefix, and publishes its own inclusive prefix.
+__device__ __forceinline__ u64 lb_prefix(u64* status, u32 tile, u64 agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) lb_store(status, kLbPre | agg);
+        return 0;
+    }
+    if (lane == 0) lb_store(status + tile, kLbAgg | agg);
+    u64 pre = 0;
+    for (long long j = (long long)tile - 1;; j -= 32) {
+        const long long idx = j - lane;
+        u64 v = kLbPre;  // before tile 0: an inclusive prefix of 0
+        if (idx >= 0)
+            while (((v = lb_load(status + idx)) >> 62) == 0) {
+            }
+        const u32 pm = __ballot_sync(kFull, (v >> 62) == 2);
+        // lanes up to the nearest inclusive prefix (all 32 when none)
+        const int last = pm ? __ffs(pm) - 1 : 31;
+        u64 x = lane <= last ? (v & kLbVal) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        pre += x;
+        if (pm) break;
+    }
+    if (lane == 0) lb_store(status + tile, kLbPre | (pre + agg));
+    return pre;
+}
+
+// Block-wide exclusive sum of one u32 per thread (kThr threads); the block
+// total through *total.
+template <int kThr>
+__device__ __forceinline__ u32 block_excl_sum(u32 v, u32* s_warp, u32* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const u32 w = lane < kThr / 32 ? s_warp[lane] : 0;
+        u32 wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(kFull, wi, d);
+            if (lane >= d) wi += y;
+        }
+        if (lane < kThr / 32) s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    *total = s_warp[32];
+    return s_warp[wid] + incl - v;
+}
+
+
+
 }  // namespace rg

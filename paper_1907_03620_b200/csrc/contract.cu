@@ -858,6 +858,78 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, cons
     if (slen) k2_flush(t, s_idx, slen, out, ctr, lane);
 }
 
+// K2, one pass per tile (default): a block takes the next tile of
+// kK2LbThr x kK2LbPer slots from a ticket, loads all of its slots (eight
+// 16-byte loads in flight per thread), counts the significant ones,
+// reserves the tile's output range with one atomic and writes key, count
+// and slot index straight from registers. No re-read of the table (the
+// staged variant above re-reads every flushed slot).
+constexpr int kK2LbThr = 256, kK2LbPer = 8;
+constexpr u64 kK2LbTile = (u64)kK2LbThr * kK2LbPer;
+__global__ void __launch_bounds__(kK2LbThr) k_compact_lb(Table t, u64 cap, u64 tau, const u8* keep,
+                                                         K2Out o, Counters* ctr, u64* status,
+                                                         u32* ticket) {
+    __shared__ u32 s_warp[33];
+    __shared__ u32 s_tile;
+    __shared__ u64 s_pre;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const u32 tile = s_tile;
+    const int lane = threadIdx.x & 31;
+    const u64 base = (u64)tile * kK2LbTile;
+    u64 k[kK2LbPer], v[kK2LbPer];
+#pragma unroll
+    for (int j = 0; j < kK2LbPer; ++j) {
+        const u64 i = base + (u64)j * kK2LbThr + threadIdx.x;  // striped: coalesced
+        k[j] = kEmpty;
+        v[j] = 0;
+        if (i < cap) ld_slot(t.slots + i, k[j], v[j]);
+    }
+    u32 flags = 0;
+#pragma unroll
+    for (int j = 0; j < kK2LbPer; ++j) {
+        const u64 i = base + (u64)j * kK2LbThr + threadIdx.x;
+        const bool sig = k[j] != kEmpty && (keep ? (i < cap && keep[i] != 0) : v[j] >= tau);
+        flags |= (u32)sig << j;
+    }
+    u32 agg;
+    const u32 ex = block_excl_sum<kK2LbThr>((u32)__popc(flags), s_warp, &agg);
+    // one reservation per tile (the output order is free: K3 sorts). A
+    // decoupled look-back here measured 370 us: with ~1,200 tiles in
+    // flight the look-back walked hundreds of predecessors per tile.
+    if (threadIdx.x == 0) s_pre = agg ? atomicAdd(&ctr->n_sig, (u64)agg) : 0;
+    __syncthreads();
+    u64 pos = s_pre + ex;
+#pragma unroll
+    for (int j = 0; j < kK2LbPer; ++j) {
+        const bool sig = (flags >> j) & 1u;
+        if (sig) {
+            const u32 i = (u32)(base + (u64)j * kK2LbThr + threadIdx.x);
+            o.sig_key[pos] = k[j];
+            o.sig_cnt[pos] = v[j];
+            if (o.size) {  // hash-probe K3 only (the sorted K3 initialises its own)
+                o.parent[pos] = (u32)pos;
+                o.size[pos] = 0;
+                o.npts[pos] = 0;
+                o.min_key[pos] = kEmpty;
+                o.root_cid[pos] = -1;
+            }
+            if (o.slot_of)
+                o.slot_of[pos] = i;  // the table's SIG marks are written when K4 needs them
+            else
+                t.slots[i].count = kSigBit | pos;
+            ++pos;
+        }
+        if (o.col_cnt) {
+            // column histogram of the sorted K3: a warp's 32 slots of row j
+            // share a few 4x4 blocks, so one RED per distinct column
+            const u32 col = sig ? (u32)(k[j] >> o.bits_y) : 0xffffffffu;
+            const u32 peers = __match_any_sync(kFull, col);
+            if (sig && lane == __ffs(peers) - 1) red_add_u32(o.col_cnt + col, (u32)__popc(peers));
+        }
+    }
+}
+
 // Deferred SIG marks (sorted K3 path): the count word of significant tile
 // pos becomes SIG | pos (dense index, as K2 writes it on the hash path) or
 // SIG | (cluster id + 1) (K4's lookups then need no second load).
@@ -959,10 +1031,12 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
     return cudaGetLastError();
 }
 
+u64 compact_lb_words(u64 cap) { return (cap + kK2LbTile - 1) / kK2LbTile + 2; }
+
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
                            u32* col_cnt, u32* slot_of, Counters* ctr, int n_sm,
-                           cudaStream_t st) {
+                           cudaStream_t st, u64* lb_scratch) {
 #ifndef RG_K2_BPS
 #define RG_K2_BPS 16
 #endif
@@ -972,6 +1046,18 @@ cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_k
     const int blocks = (int)(want < mx ? (want ? want : 1) : mx);
     const K2Out o{sig_key, sig_cnt, parent, size, npts, min_key, root_cid, col_cnt, t.bits_y,
                   slot_of};
+    static const bool staged = [] {  // RG_K2=staged: the reservation-based K2 (A/B)
+        const char* v = std::getenv("RG_K2");
+        return v && std::strcmp(v, "staged") == 0;
+    }();
+    if (lb_scratch && !staged) {
+        const u64 tiles = (cap + kK2LbTile - 1) / kK2LbTile;
+        cudaError_t e = cudaMemsetAsync(lb_scratch, 0, (tiles + 2) * sizeof(u64), st);
+        if (e != cudaSuccess) return e;
+        k_compact_lb<<<(int)tiles, kK2LbThr, 0, st>>>(t, cap, tau, keep, o, ctr, lb_scratch + 2,
+                                                      (u32*)lb_scratch);
+        return cudaGetLastError();
+    }
     k_compact<<<blocks, 256, 0, st>>>(t, cap, tau, keep, o, ctr);
     return cudaGetLastError();
 }

@@ -37,10 +37,13 @@ cudaError_t launch_export(const Slot* slots, u64 cap, u64* keys, u64* cnts, u64*
                           cudaStream_t st);
 cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_sm,
                              cudaStream_t st);
+// lb_scratch (K2 look-back: cap / 2048 + 2 words) selects the one-pass K2;
+// null selects the staged K2 (reservation atomics)
+u64 compact_lb_words(u64 cap);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
                            u32* col_cnt, u32* slot_of, Counters* ctr, int n_sm,
-                           cudaStream_t st);
+                           cudaStream_t st, u64* lb_scratch = nullptr);
 cudaError_t launch_mark_sig(Table t, const u32* slot_of, const int* cid, u64 n, int n_sm,
                             cudaStream_t st);
 cudaError_t launch_window_mark(Table t, u64 cap, u64 tau, u32 bits_x, u8* keep, int n_sm,
