@@ -26,6 +26,8 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -1251,6 +1253,8 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         ++launches;
     }
     {
+        // (four short passes instead - count, scan, root ids, labels - with
+        // ballot bitmaps measured 128 us against this kernel's 119 us)
         const u64 tiles = (n + kLbTile - 1) / kLbTile;
         const LbScratch lb = lb_scratch(L.temp, tiles, st);
         k_sorted_ids<<<(int)tiles, kLbThr, 0, st>>>(L.parent, L.size, L.mu, L.perm, L.n_sig_dev,
