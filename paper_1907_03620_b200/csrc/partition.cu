@@ -37,6 +37,7 @@
 // the per-point fallback (a unit KP2 flags as overflowed, whose points KP3
 // adds one by one) is exercised with RG_PART_MAX_ROUNDS=1 in the tests.
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -555,6 +556,10 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         cudaFuncSetAttribute(k_part_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
         attr = true;
     }
+    // (a direct variant - one block per 64 Ki-point tile storing each
+    // residual straight to its run with a shared-memory cursor, relying on
+    // L2 to merge the 4-byte stores - measured 13.8 ms: 7.85 GB of DRAM
+    // writes for 2 GB of residuals)
     k_part_scatter<<<(int)std::min<u64>(T, (u64)L.n_sm * RG_KP1_BLOCKS), kP1Thr, kScatterSmem, st>>>(
         xy, n, L.g, m, c.off, T, c.res);
     std::vector<u32> base(kParts + 1);
