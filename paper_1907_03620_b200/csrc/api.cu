@@ -364,6 +364,7 @@ struct rg_ctx {
     u64* pair_key = nullptr;
     u32* pair_cnt = nullptr;
     u64 pair_cap = 0;
+    int part_stream_hint = 0;  // 1: the one-pass scatter fell back for the probed buffer
     u64 order_probe[3] = {0, 0, 0};
     u64 probe_fp = 0;       // fingerprint of the probed buffer's content
     u64* k2_lb = nullptr;   // K2's look-back status words
@@ -696,8 +697,8 @@ void resolve_contract_timer(rg_ctx* ctx) {
 // accumulator.hpp:120-134). Handles budget stops, growth and resumption.
 // Inputs without spatial order take the partitioned contraction
 // (partition.cu). RG_INGEST=k1 / =part forces a path; otherwise a probe of
-// 64 windows of 4096 consecutive points decides: when more than a quarter
-// of a window's points open a new tile, K1's per-warp cache cannot help.
+// 64 windows of 2,048 consecutive points decides: when more than 60 % of a
+// window's points open a new tile, K1's per-warp cache cannot help.
 bool buffer_unordered(rg_ctx* ctx, const double* xy, u64 n);
 
 bool use_partition_ingest(rg_ctx* ctx, const double* xy, u64 n) {
@@ -759,13 +760,15 @@ rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
         CK(cudaMalloc(&ctx->part_scratch, need));
         ctx->part_scratch_bytes = need;
     }
-    if (ctx->pair_cap < n) {  // one pair slot per point: per-unit slabs never overlap
+    // one pair slot per residual entry: per-unit slabs never overlap
+    const u64 pair_need = partition_res_entries(n);
+    if (ctx->pair_cap < pair_need) {
         dfree(ctx->pair_key);
         dfree(ctx->pair_cnt);
         ctx->pair_cap = 0;
-        CK(dalloc(&ctx->pair_key, n));
-        CK(dalloc(&ctx->pair_cnt, n));
-        ctx->pair_cap = n;
+        CK(dalloc(&ctx->pair_key, pair_need));
+        CK(dalloc(&ctx->pair_cnt, pair_need));
+        ctx->pair_cap = pair_need;
     }
     PartitionPlan plan;
     PhaseTimer timer(ctx, &ctx->ms_contract);
@@ -780,8 +783,12 @@ rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
     L.pkey = ctx->pair_key;
     L.pcnt = ctx->pair_cnt;
     L.n_sm = ctx->n_sm;
+    L.narrow = ctx->narrow;
+    // the one-pass scatter's fallback is remembered with the order verdict
+    if (!(ctx->probe_ptr == xy && ctx->probe_n == n)) ctx->part_stream_hint = 0;
+    L.stream_hint = &ctx->part_stream_hint;
     CK(launch_partition_count(L, ctx->st, &plan));
-    ctx->launches += 5;  // hist, scan (2), scatter, aggregate
+    ctx->launches += plan.launches;
     const u64 pairs = plan.pair_off.back();
     // the table must hold every key KP3 can claim below the load target
     while ((double)(ctx->used + pairs + plan.raw_points) >= kMaxLoad * (double)ctx->cap) {

@@ -199,6 +199,37 @@ __device__ __forceinline__ bool table_add_cas(const Table& t, u64 key, u64 cnt) 
     }
 }
 
+// table_add_cas with one 128-bit CAS that installs key and count together
+// ({EMPTY, 0} is the cleared state): a new key costs a single atomic and no
+// RED. Faster where most keys are new (KP3's pair inserts, config 5's noise);
+// slower for K1's evictions on config 4 (1.586 against 1.550 ms), which keep
+// the 64-bit claim.
+__device__ __forceinline__ bool table_add_cas128(const Table& t, u64 key, u64 cnt) {
+    Probe p(key, t);
+    Slot want, empty;
+    want.key = key;
+    want.count = cnt;
+    empty.key = kEmpty;
+    empty.count = 0;
+    while (true) {
+        Slot* s = t.slots + p.slot();
+        const Slot old = atomicCAS(s, empty, want);
+        if (old.key == kEmpty && old.count == 0) return true;
+        if (old.key == key) {
+            red_add(&s->count, cnt);
+            return false;
+        }
+        if (old.key == kEmpty) {  // defensive: an empty key with a count takes the 64-bit claim
+            const u64 o2 = atomicCAS(&s->key, kEmpty, key);
+            if (o2 == kEmpty || o2 == key) {
+                red_add(&s->count, cnt);
+                return o2 == kEmpty;
+            }
+        }
+        p.next(t);
+    }
+}
+
 // Lookup: returns the slot's value word, or kEmpty when the key is absent.
 // TileCounts::count_of accumulator.hpp:53-61.
 __device__ __forceinline__ u64 table_find(const Table& t, u64 key) {
@@ -242,6 +273,13 @@ struct KeyOps<true> {
         const u32 ky = (u32)(ty - g.oy32);
         return in_bounds(g, x, y) ? (((u64)kx << 32) | ky) : kEmpty;
     }
+    // The key without the bounds select (any value for an out-of-bounds
+    // point: callers carry the bounds predicate separately).
+    __device__ static __forceinline__ u64 raw_key(const Grid& g, double x, double y) {
+        const int tx = __double2int_rd(__dmul_rn(x, g.scale));
+        const int ty = __double2int_rd(__dmul_rn(y, g.scale));
+        return ((u64)(u32)(tx - g.ox32) << 32) | (u32)(ty - g.oy32);
+    }
     // Direct-mapped by position in an 8 x 16-tile window (low 3 column bits,
     // low 4 row bits): the few tiles of one cluster never evict each other.
     __device__ static __forceinline__ u32 slot(u64 ck, u32) {
@@ -257,6 +295,9 @@ struct KeyOps<false> {
     __device__ static __forceinline__ u64 cache_key(const Grid& g, double x, double y) {
         const u64 k = pack_key(g, x, y);
         return in_bounds(g, x, y) ? k : kEmpty;
+    }
+    __device__ static __forceinline__ u64 raw_key(const Grid& g, double x, double y) {
+        return pack_key(g, x, y);
     }
     __device__ static __forceinline__ u32 slot(u64 k, u32 bits_y) {
         return (((u32)(k >> bits_y) & 7u) << 4) | ((u32)k & 15u);

@@ -136,9 +136,9 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
 // 1, and the others (a different key won the slot in this row) stage
 // (key, 1) themselves.
 template <bool kNarrow>
-__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const double* x,
+__device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
-                                              int lane, u32 lt_mask) {
+                                              int lane, u32 lt_mask, u32 budget) {
     using K = KeyOps<kNarrow>;
     u64 key[kBatch];
     u32 cs[kBatch];
@@ -190,43 +190,46 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
             if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
         }
     }
+    return s.pot >= budget;
 }
 #else
 // One batch of kBatch rows already in registers (one point per lane per
 // row). Every lane looks its tiles up in the per-warp cache; a hit adds 1
 // with a shared-memory increment (fire-and-forget: the warp does not wait,
 // and lanes of one tile are aggregated in the shared-memory atomic unit).
-// The lookups are branch-free (the slot of an out-of-bounds point is a
-// valid index, its kEmpty key never hits). Misses of ALL rows of the batch
+// The lookups are branch-free: the bounds test stays a predicate (an
+// out-of-bounds point's key is never materialised or compared against the
+// sentinel; its slot is still a valid index). Misses of ALL rows of the batch
 // are then resolved together, per slot: one missing (lane, row) wins the
 // slot, evicts the old occupant into the staging list (or leaves a
 // placeholder if the slot was empty) and installs its key with count 0;
 // every missing point whose key now owns its slot adds 1, the others stage
 // (key, 1). Each winner and each loser adds one staged entry.
 template <bool kNarrow>
-__device__ __forceinline__ void process_batch(const Grid& g, const Table& t, const double* x,
+__device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
-                                              int lane, u32 lt_mask) {
+                                              int lane, u32 lt_mask, u32 budget) {
     using K = KeyOps<kNarrow>;
     u64 key[kBatch];
     u32 cs[kBatch];
     bool miss[kBatch];
+    bool valid[kBatch];
 #pragma unroll
     for (int r = 0; r < kBatch; ++r) {
-        key[r] = K::cache_key(g, x[r], y[r]);
+        key[r] = K::raw_key(g, x[r], y[r]);
+        valid[r] = in_bounds(g, x[r], y[r]);
         cs[r] = K::slot(key[r], g.bits_y);
     }
     bool any = false;
 #pragma unroll
     for (int r = 0; r < kBatch; ++r) {
         const u64 ck = w.ckey[cs[r]];
-        const bool valid = key[r] != kEmpty;
-        const bool hit = (ck == key[r]) & valid;
+        const bool hit = (ck == key[r]) & valid[r];
         if (hit) atomicAdd(&w.ccnt[cs[r]], 1u);
-        miss[r] = valid & !hit;
+        miss[r] = valid[r] & !hit;
         any |= miss[r];
     }
-    if (!__any_sync(kFull, any)) return;
+    if (!__any_sync(kFull, any)) return false;  // pot only grows on the miss path
 #pragma unroll
     for (int r = 0; r < kBatch; ++r)
         if (miss[r]) w.owner[cs[r]] = (unsigned char)(r * 32 + lane);
@@ -273,6 +276,7 @@ __device__ __forceinline__ void process_batch(const Grid& g, const Table& t, con
     s.slen = pos;
     __syncwarp();
     if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
+    return s.pot >= budget;
 }
 #endif  // RG_K1_ROWWISE
 
@@ -321,6 +325,10 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
 #define RG_K1_RING 4
 #endif
 constexpr int kRing = RG_K1_RING;  // rows in flight per warp (multiple of kBatch)
+#ifndef RG_K1_UNROLL
+#define RG_K1_UNROLL 2
+#endif
+constexpr int kK1Unroll = RG_K1_UNROLL;  // batches per trip of run_segment's loop
 
 // One segment of nr rows starting at `base` (this lane's point of the first
 // row). kFullRows: every point of every row exists (all segments but
@@ -351,6 +359,7 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
     };
 #pragma unroll
     for (int k = 0; k < kRing; ++k) issue(k);
+#pragma unroll kK1Unroll
     for (u32 j = 0; j < nr; j += kBatch) {
         cp_async_wait<kRing - kBatch>();
         double x[kBatch], y[kBatch];
@@ -370,10 +379,11 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
 #ifdef RG_K1_STREAM_ONLY  // experiment: the load path alone (results are wrong)
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) st.added += (x[b] + y[b] > 1e300) ? 1 : 0;
+        const bool over = false;
 #else
-        process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask);
+        const bool over = process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask, budget);
 #endif
-        if (st.pot >= budget) return j + kBatch < nr ? j + kBatch : nr;
+        if (over) return j + kBatch < nr ? j + kBatch : nr;
     }
     return nr;
 }
@@ -417,8 +427,7 @@ __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 v
 #endif
             issue(b + kStages);
         }
-        process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask);
-        if (st.pot >= budget) {
+        if (process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask, budget)) {
             done_b = b + 1;
             break;
         }

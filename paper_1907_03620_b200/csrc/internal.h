@@ -154,7 +154,10 @@ struct PartitionLaunch {
     u64* pkey;          // n entries: (key, count) pairs, one slab per work unit
     u32* pcnt;
     int n_sm;
+    bool narrow;        // canvas indices fit int32 (32-bit projection)
+    int* stream_hint;   // caller-owned memo: 1 = the one-pass scatter fell back last time
 };
+u64 partition_res_entries(u64 n);
 bool partition_ingest_supported(u32 key_bits, u64 n);
 size_t partition_scratch_bytes(u64 n, size_t* scan_temp);
 cudaError_t launch_order_probe(const double* xy, u64 n, Grid g, u64* out, int n_sm,
@@ -165,6 +168,7 @@ struct PartitionPlan {
     std::vector<u64> pair_off;  // exclusive prefix of dcnt (overflowed units add 0)
                                 // (pairs live in per-unit slabs at units[u].x)
     u64 raw_points = 0;         // points of overflowed units (added one by one)
+    int launches = 0;           // kernels launched by launch_partition_count
 };
 cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, PartitionPlan* plan);
 cudaError_t launch_partition_insert(const PartitionLaunch& L, Table t, const PartitionPlan& plan,

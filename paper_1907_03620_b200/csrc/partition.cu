@@ -33,9 +33,11 @@
 // A partition is the low 11 bits of a bijective mix of the packed key
 // (multiply by an odd constant mod 2^B, then xor-shift by ceil(B/2)); the
 // other B-11 bits are the residual, so the key is recovered exactly. A unit
-// holds at most 256 Ki points, so 32 rounds of 12 Ki tiles always suffice;
+// holds at most 512 Ki points, so 64 rounds of 12 Ki tiles always suffice;
 // the per-point fallback (a unit KP2 flags as overflowed, whose points KP3
 // adds one by one) is exercised with RG_PART_MAX_ROUNDS=1 in the tests.
+#include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -268,6 +270,242 @@ __global__ void __launch_bounds__(kP1Thr, RG_KP1_BLOCKS) k_part_scatter(const do
     }
 }
 
+// ------------------------------------------------------------------ KQ path
+// One-pass scatter for inputs whose points spread evenly over the partitions
+// (any input without a hot tile). KP0's exact histogram costs a full read of
+// the points (1.3 ms of config 4's 8 GB); here a strided sample sizes the
+// regions instead:
+//
+//   KQ0 k_part_sample  every stride-th point -> sampled points per partition;
+//   KQp k_part_plan    per partition a region of nblk equal sub-regions (one
+//                      per KQ1 block), each sized estimate + 6 sigma (sampling
+//                      and thinning noise) and a multiple of 8 entries; falls
+//                      back to the exact path when a partition is hot or the
+//                      regions exceed the scratch;
+//   KQ1 k_part_stream  one 1024-thread block per SM streams its rounds of
+//                      8192 points once (the next round's loads are in flight
+//                      while a round is processed) into per-partition
+//                      write-combining buffers in shared memory (24 entries
+//                      each); after every round the full groups of 8 entries
+//                      leave as whole aligned 32-byte sectors to the block's
+//                      own sub-region (no global atomics, no partial-sector
+//                      writes), the rest (< 8) stays for the next round. At
+//                      the end the tails and the unused part of every
+//                      sub-region are filled with the skip marker KP2 ignores.
+//
+// A sub-region that overflows (the estimate was wrong) raises a flag and the
+// call is redone on the exact path, so the result never depends on the
+// sample.
+constexpr u32 kQC = 24;                 // entries per write-combining buffer
+constexpr int kQThr = 1024;
+constexpr int kQPer = 8;                // points per thread per round
+constexpr u32 kQRound = kQThr * kQPer;  // 8192
+constexpr u32 kQHot = 6;                // expected points per partition and round above which the exact path is taken
+constexpr size_t kStreamSmem = (size_t)(kParts * kQC + 4 * kParts) * 4;
+constexpr u32 kSkip = 0xffffffffu;
+
+// plan words (u32) after the kParts + 1 sample counters
+enum : u32 { kPlFallback = 0, kPlOverflow = 1, kPlWords = 4 };
+
+__global__ void __launch_bounds__(256) k_part_sample(const double2* xy, u64 n, Grid g, Mix m,
+                                                     u64 stride, u32* shist) {
+    __shared__ u32 hist[kParts + 1];
+    for (u32 i = threadIdx.x; i <= kParts; i += 256) hist[i] = 0;
+    __syncthreads();
+    const u64 ns = (n + stride - 1) / stride;
+    for (u64 s0 = blockIdx.x * 256ull + threadIdx.x; s0 < ns; s0 += (u64)gridDim.x * 256) {
+        // offset by a per-sample hash so a periodic input cannot alias with the stride
+        const u64 i = min(n - 1, s0 * stride + ((s0 * 0x9E3779B97F4A7C15ull) >> 40) % stride);
+        u64 k;
+        if (point_key(g, xy[i], k)) {
+            atomicAdd(&hist[(u32)mix(m, k) & (kParts - 1)], 1u);
+            atomicAdd(&hist[kParts], 1u);
+        }
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i <= kParts; i += 256)
+        if (hist[i]) atomicAdd(&shist[i], hist[i]);
+}
+
+// One block: capacities, region starts, fallback decision.
+//   capb[p]   entries of one block's sub-region of partition p (multiple of 8)
+//   pstart[p] first entry of partition p's region; pstart[kParts] = total
+__global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 stride, u32 nblk,
+                                                    u64 res_cap, float sigmas, u32* capb,
+                                                    u32* pstart, u32* plan) {
+    __shared__ u64 tot[kParts];
+    __shared__ u32 smax;
+    if (threadIdx.x == 0) smax = 0;
+    __syncthreads();
+    u32 mx = 0;
+    for (u32 p = threadIdx.x; p < kParts; p += 1024) {
+        const u32 sp = shist[p];
+        mx = max(mx, sp);
+        const float est = (float)sp * (float)stride / (float)nblk;
+        const float sd = sqrtf(est * (1.0f + (float)stride / (float)nblk));
+        const u32 c = ((u32)(est + sigmas * sd) + 16 + 7) & ~7u;
+        capb[p] = c;
+        tot[p] = (u64)c * nblk;
+    }
+    atomicMax(&smax, mx);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 run = 0;
+        bool big = false;
+        for (u32 p = 0; p < kParts; ++p) {
+            pstart[p] = (u32)run;
+            run += tot[p];
+            big |= run > res_cap;
+        }
+        pstart[kParts] = big ? 0u : (u32)run;
+        const u64 S = shist[kParts];
+        const bool hot = (u64)smax * kQRound > (u64)kQHot * S;
+        plan[kPlFallback] = big ? 2u : (hot ? 1u : 0u);
+        plan[kPlOverflow] = 0;
+    }
+}
+
+struct StreamArgs {
+    const double2* xy;
+    u64 n;
+    Grid g;
+    Mix m;
+    const u32* capb;
+    const u32* pstart;
+    u32* plan;
+    u32* res;
+    u64* inout;  // [0] in-bounds points, [1] skipped points (added to the counters on success)
+};
+
+template <bool kNarrow>
+__device__ __forceinline__ u64 stream_key(const Grid& g, double2 v) {
+    if (kNarrow) {
+        const u64 ck = KeyOps<true>::raw_key(g, v.x, v.y);
+        return ((ck >> 32) << g.bits_y) | (u32)ck;
+    }
+    return pack_key(g, v.x, v.y);
+}
+
+template <bool kNarrow>
+__global__ void __launch_bounds__(kQThr, 1) k_part_stream(StreamArgs A) {
+    extern __shared__ u32 sh_q[];
+    u32* buf = sh_q;                    // kParts x kQC residuals
+    u32* cnt = buf + kParts * kQC;      // entries waiting per partition
+    u32* bcur = cnt + kParts;           // next entry of this block's sub-region
+    u32* bend = bcur + kParts;          // end of this block's sub-region
+    u32* list = bend + kParts;          // partitions with a full sector this round
+    __shared__ u32 nlist;
+    if (A.plan[kPlFallback]) return;    // the plan chose the exact path
+    const u32 tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const u32 nblk = gridDim.x, b = blockIdx.x;
+    for (u32 p = tid; p < kParts; p += kQThr) {
+        cnt[p] = 0;
+        bcur[p] = A.pstart[p] + b * A.capb[p];
+        bend[p] = A.pstart[p] + (b + 1) * A.capb[p];
+    }
+    if (tid == 0) nlist = 0;
+    const u64 pol = evict_first_policy();
+    const double2 nanpt = make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
+    const u64 n = A.n, n_rounds = (n + kQRound - 1) / kQRound;
+    const Grid g = A.g;
+    const Mix m = A.m;
+    u64 in = 0, seen = 0;
+    bool over = false;
+    double2 v[kQPer];
+#pragma unroll
+    for (int j = 0; j < kQPer; ++j) {
+        const u64 i = (u64)b * kQRound + (u64)j * kQThr + tid;
+        v[j] = (b < n_rounds && i < n) ? ld_point_stream(A.xy + i, pol) : nanpt;
+    }
+    __syncthreads();
+    for (u64 r = b; r < n_rounds; r += nblk) {
+        const u64 nx = r + nblk;
+        {
+            const u64 base = r * kQRound + tid;
+            const u64 left = n > base ? n - base : 0;  // points j with j * kQThr < left exist
+            seen += min((u64)kQPer, (left + kQThr - 1) / kQThr);
+        }
+#pragma unroll
+        for (int j = 0; j < kQPer; ++j) {
+            const double2 pt = v[j];
+            const u64 i = nx * kQRound + (u64)j * kQThr + tid;
+            v[j] = (nx < n_rounds && i < n) ? ld_point_stream(A.xy + i, pol) : nanpt;
+            if (in_bounds(g, pt.x, pt.y)) {
+                const u64 h = mix(m, stream_key<kNarrow>(g, pt));
+                const u32 p = (u32)h & (kParts - 1);
+                const u32 rr = (u32)(h >> kPBits);
+                const u32 rank = atomicAdd(&cnt[p], 1u);
+                if (rank < kQC) {
+                    buf[p * kQC + rank] = rr;
+                } else {  // buffer full (rare): straight to the sub-region
+                    const u32 at = atomicAdd(&bcur[p], 1u);
+                    if (at < bend[p]) A.res[at] = rr;
+                    else over = true;
+                }
+                ++in;
+            }
+        }
+        __syncthreads();
+        // partitions with at least one full sector
+#pragma unroll
+        for (int q = 0; q < (int)(kParts / kQThr); ++q) {
+            const u32 p = q * kQThr + tid;
+            const u32 c = cnt[p];
+            if (c > kQC) cnt[p] = kQC;
+            const u32 msk = __ballot_sync(kFull, c >= 8);
+            u32 at = 0;
+            if (lane == 0 && msk) at = atomicAdd(&nlist, (u32)__popc(msk));
+            at = __shfl_sync(kFull, at, 0);
+            if (c >= 8) list[at + __popc(msk & ((1u << lane) - 1))] = p;
+        }
+        __syncthreads();
+        {
+            const u32 nl = nlist, l = lane & 7, grp = lane >> 3;
+            for (u32 e0 = wid * 4; e0 < nl; e0 += (kQThr / 32) * 4) {
+                const u32 e = e0 + grp;
+                if (e < nl) {
+                    const u32 p = list[e];
+                    const u32 c = cnt[p], nfl = c & ~7u, base = bcur[p];
+                    const bool ok = base + nfl <= bend[p];
+                    if (ok)
+                        for (u32 j = 0; j < nfl; j += 8) A.res[base + j + l] = buf[p * kQC + j + l];
+                    else
+                        over = true;
+                    // the tail (< 8 entries, beyond the flushed part) moves to the front
+                    if (l < c - nfl) buf[p * kQC + l] = buf[p * kQC + nfl + l];
+                    if (l == 0) {
+                        cnt[p] = c - nfl;
+                        if (ok) bcur[p] = base + nfl;
+                    }
+                }
+            }
+        }
+        if (tid == 0) nlist = 0;
+        __syncthreads();
+    }
+    // tails, then the skip marker through the end of every sub-region
+    for (u32 p = wid; p < kParts; p += kQThr / 32) {
+        const u32 c = min(cnt[p], kQC), base = bcur[p];
+        const u32 end = bend[p];
+        if (base + c > end) over = true;
+        for (u32 i = lane; base + i < end; i += 32) A.res[base + i] = i < c ? buf[p * kQC + i] : kSkip;
+    }
+    if (__any_sync(kFull, over) && lane == 0) A.plan[kPlOverflow] = 1;
+    u64 out = seen - in;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        in += __shfl_xor_sync(kFull, in, o);
+        out += __shfl_xor_sync(kFull, out, o);
+    }
+    if (lane == 0 && in) atomicAdd(&A.inout[0], in);
+    if (lane == 0 && out) atomicAdd(&A.inout[1], out);
+}
+
+__global__ void k_part_commit(Counters* ctr, const u64* inout) {
+    if (inout[0]) atomicAdd(&ctr->ingested, inout[0]);
+    if (inout[1]) atomicAdd(&ctr->skipped, inout[1]);
+}
+
 // Round of a residual when a unit's tiles do not fit one shared-memory
 // table: rounds split the residuals by a hash, R rounds (a power of two).
 __device__ __forceinline__ u32 round_of(u32 r, u32 R) { return ((r * 0x85EBCA6Bu) >> 16) & (R - 1); }
@@ -394,7 +632,7 @@ __global__ void __launch_bounds__(256) k_part_insert(const uint4* units, u32 n_u
         if (d == kOverflow) continue;
         const u64 lo = units[u].x;
         for (u32 i = threadIdx.x; i < d; i += blockDim.x)
-            claims += table_add_cas(t, pkey[lo + i], pcnt[lo + i]) ? 1u : 0u;
+            claims += table_add_cas128(t, pkey[lo + i], pcnt[lo + i]) ? 1u : 0u;
     }
     claims = __reduce_add_sync(kFull, claims);
     if ((threadIdx.x & 31) == 0 && claims) atomicAdd(&ctr->used, (u64)claims);
@@ -461,22 +699,31 @@ bool partition_ingest_supported(u32 key_bits, u64 n) {
     return key_bits >= 20 && key_bits <= 42 && n < (1ull << 31);
 }
 
-constexpr u32 kUnit = 1u << 18;  // points per KP2 work unit (hot partitions are split)
+constexpr u32 kUnit = 1u << 19;  // entries per KP2 work unit (hot partitions are split)
 
 u64 max_units(u64 n) { return kParts + n / kUnit + 2; }
 
-// scratch: residuals (4 B / point), per-(partition, tile) counts and
-// offsets, partition bases, work units with their rounds / distinct counts /
-// pair offsets, scan temp.
+// Residual entries the scratch holds: the one-pass scatter's regions are
+// estimates with head-room (k_part_plan), the exact path needs n.
+// (6 sigma of a sub-region over <= 160 blocks x 2048 partitions adds up to
+// about 4,600 sqrt(n) entries; 24 per sub-region for rounding and padding)
+u64 partition_res_entries(u64 n) {
+    return n + (u64)(4800.0 * std::sqrt((double)n)) + (u64)kParts * 160 * 24 + 4096;
+}
+
+// scratch: residuals (4 B / entry), per-(partition, tile) counts and
+// offsets, partition bases, the one-pass plan (sample counters, capacities,
+// region starts, flags, counters), work units with their rounds / distinct
+// counts / pair offsets, scan temp.
 size_t partition_scratch_bytes(u64 n, size_t* scan_temp) {
     const u64 T = (n + kPTile - 1) / kPTile;
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum((void*)nullptr, tb, (const u32*)nullptr, (u32*)nullptr,
                                   (int)(kParts * T + 1));
     *scan_temp = tb;
-    const u64 U = max_units(n);
-    return n * 4 + 2 * (kParts * T + 1) * 4 + (kParts + 1) * 4 + U * 16 + 2 * U * 4 +
-           (U + 1) * 8 + tb + 4096;
+    const u64 U = max_units(partition_res_entries(n));
+    return partition_res_entries(n) * 4 + 2 * (kParts * T + 1) * 4 + (kParts + 1) * 4 +
+           (3 * kParts + 2 + kPlWords + 4) * 4 + 64 + U * 16 + 2 * U * 4 + (U + 1) * 8 + tb + 4096;
 }
 
 u32 partition_count() { return kParts; }
@@ -496,24 +743,36 @@ cudaError_t launch_order_probe(const double* xy, u64 n, Grid g, u64* out, int n_
 namespace {
 struct Carve {
     u32 *res, *hist, *off, *base, *rounds, *dcnt;
+    u32 *shist, *capb, *pstart, *plan;  // one-pass scatter
+    u64* inout;
     uint4* units;
     u64* pair_off;
     void* temp;
 };
 Carve carve(void* scratch, u64 n) {
     const u64 T = (n + kPTile - 1) / kPTile;
-    const u64 U = max_units(n);
+    const u64 U = max_units(partition_res_entries(n));
     Carve c;
     char* w = (char*)scratch;
     c.res = (u32*)w;
-    w += n * 4;
+    w += partition_res_entries(n) * 4;
     c.hist = (u32*)w;
     w += (kParts * T + 1) * 4;
     c.off = (u32*)w;
     w += (kParts * T + 1) * 4;
     c.base = (u32*)w;
     w += (kParts + 1) * 4;
+    c.shist = (u32*)w;  // kParts + 1 sample counters, then the plan words (cleared together)
+    w += (kParts + 1) * 4;
+    c.plan = (u32*)w;
+    w += kPlWords * 4;
+    c.capb = (u32*)w;
+    w += kParts * 4;
+    c.pstart = (u32*)w;
+    w += (kParts + 1) * 4;
     w = (char*)(((uintptr_t)w + 15) & ~(uintptr_t)15);
+    c.inout = (u64*)w;
+    w += 2 * 8;
     c.units = (uint4*)w;
     w += U * 16;
     c.rounds = (u32*)w;
@@ -537,36 +796,99 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
     const Carve c = carve(L.scratch, n);
     const double2* xy = reinterpret_cast<const double2*>(L.xy);
     cudaError_t e;
-    if ((e = cudaMemsetAsync(c.hist + kParts * T, 0, 4, st)) != cudaSuccess) return e;
-    const int g0 = (int)std::min<u64>(T, (u64)L.n_sm * 4);
-    k_part_hist<<<g0, kPThreads, 0, st>>>(xy, n, L.g, m, c.hist, T, L.ctr);
-    size_t tb = L.scan_temp;
-    if ((e = cub::DeviceScan::ExclusiveSum(c.temp, tb, c.hist, c.off, (int)(kParts * T + 1), st)) !=
-        cudaSuccess)
-        return e;
-    // partition bases: off[p * T] (the total is off[kParts * T])
-    if ((e = cudaMemcpy2DAsync(c.base, 4, c.off, T * 4, 4, kParts + 1, cudaMemcpyDeviceToDevice,
-                               st)) != cudaSuccess)
-        return e;
     static bool attr = false;
     const int sm2 = (int)(2 * kAggSlots * sizeof(u32));
     if (!attr) {
         cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kScatterSmem);
         cudaFuncSetAttribute(k_part_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2);
+        cudaFuncSetAttribute(k_part_stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kStreamSmem);
+        cudaFuncSetAttribute(k_part_stream<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kStreamSmem);
         attr = true;
     }
-    // (a direct variant - one block per 64 Ki-point tile storing each
-    // residual straight to its run with a shared-memory cursor, relying on
-    // L2 to merge the 4-byte stores - measured 13.8 ms: 7.85 GB of DRAM
-    // writes for 2 GB of residuals)
-    k_part_scatter<<<(int)std::min<u64>(T, (u64)L.n_sm * RG_KP1_BLOCKS), kP1Thr, kScatterSmem, st>>>(
-        xy, n, L.g, m, c.off, T, c.res);
+    // RG_PART=exact / =stream forces the scatter (stream still falls back
+    // when its plan says so); the parity tests run both.
+    static const int forced = [] {
+        const char* v = std::getenv("RG_PART");
+        return v ? (std::strcmp(v, "exact") == 0 ? 1 : (std::strcmp(v, "stream") == 0 ? 2 : 0)) : 0;
+    }();
+    static const bool debug = std::getenv("RG_DEBUG") != nullptr;
+    // head-room of a sub-region in standard deviations (RG_PART_SIGMA: test
+    // knob; a negative value makes sub-regions overflow so the fallback runs)
+    static const float sigmas = [] {
+        const char* v = std::getenv("RG_PART_SIGMA");
+        return v ? (float)std::atof(v) : 6.0f;
+    }();
     std::vector<u32> base(kParts + 1);
-    if ((e = cudaMemcpyAsync(base.data(), c.base, (kParts + 1) * 4, cudaMemcpyDeviceToHost, st)) !=
-        cudaSuccess)
-        return e;
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    bool streamed = false;
+    plan->launches = 0;
+    if (forced != 1 && !(L.stream_hint && *L.stream_hint == 1 && forced != 2)) {
+        // one-pass scatter: sample, plan, stream
+        const u64 n_rounds = (n + kQRound - 1) / kQRound;
+        const u32 nblk = (u32)std::min<u64>((u64)L.n_sm, std::max<u64>(1, n_rounds / 8));
+        const u64 stride = std::min<u64>(128, std::max<u64>(1, n >> 18));
+        const u64 res_cap = std::min<u64>(partition_res_entries(n), 0xfffffff0ull);
+        if ((e = cudaMemsetAsync(c.shist, 0, (kParts + 1 + kPlWords) * 4, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(c.inout, 0, 16, st)) != cudaSuccess) return e;
+        const u64 ns = (n + stride - 1) / stride;
+        k_part_sample<<<(int)std::min<u64>((ns + 255) / 256, (u64)L.n_sm * 8), 256, 0, st>>>(
+            xy, n, L.g, m, stride, c.shist);
+        k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, nblk, res_cap, sigmas, c.capb, c.pstart,
+                                        c.plan);
+        StreamArgs A{xy, n, L.g, m, c.capb, c.pstart, c.plan, c.res, c.inout};
+        if (L.narrow)
+            k_part_stream<true><<<(int)nblk, kQThr, kStreamSmem, st>>>(A);
+        else
+            k_part_stream<false><<<(int)nblk, kQThr, kStreamSmem, st>>>(A);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        plan->launches += 3;
+        u32 flags[kPlWords];
+        if ((e = cudaMemcpyAsync(flags, c.plan, sizeof(flags), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            return e;
+        if ((e = cudaMemcpyAsync(base.data(), c.pstart, (kParts + 1) * 4, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        streamed = flags[kPlFallback] == 0 && flags[kPlOverflow] == 0;
+        if (debug)
+            std::fprintf(stderr, "[rg] one-pass scatter n=%llu blocks=%u stride=%llu: %s\n",
+                         (unsigned long long)n, nblk, (unsigned long long)stride,
+                         streamed ? "ok"
+                                  : (flags[kPlFallback] == 1 ? "hot partition -> exact path"
+                                     : flags[kPlFallback] == 2 ? "regions exceed the scratch -> exact path"
+                                                               : "sub-region overflow -> exact path"));
+        if (L.stream_hint) *L.stream_hint = streamed ? 0 : 1;
+        if (streamed) {
+            k_part_commit<<<1, 1, 0, st>>>(L.ctr, c.inout);
+            plan->launches += 1;
+        }
+    }
+    if (!streamed) {
+        if ((e = cudaMemsetAsync(c.hist + kParts * T, 0, 4, st)) != cudaSuccess) return e;
+        const int g0 = (int)std::min<u64>(T, (u64)L.n_sm * 4);
+        k_part_hist<<<g0, kPThreads, 0, st>>>(xy, n, L.g, m, c.hist, T, L.ctr);
+        size_t tb = L.scan_temp;
+        if ((e = cub::DeviceScan::ExclusiveSum(c.temp, tb, c.hist, c.off, (int)(kParts * T + 1), st)) !=
+            cudaSuccess)
+            return e;
+        // partition bases: off[p * T] (the total is off[kParts * T])
+        if ((e = cudaMemcpy2DAsync(c.base, 4, c.off, T * 4, 4, kParts + 1, cudaMemcpyDeviceToDevice,
+                                   st)) != cudaSuccess)
+            return e;
+        // (a direct variant - one block per 64 Ki-point tile storing each
+        // residual straight to its run with a shared-memory cursor, relying on
+        // L2 to merge the 4-byte stores - measured 13.8 ms: 7.85 GB of DRAM
+        // writes for 2 GB of residuals)
+        k_part_scatter<<<(int)std::min<u64>(T, (u64)L.n_sm * RG_KP1_BLOCKS), kP1Thr, kScatterSmem, st>>>(
+            xy, n, L.g, m, c.off, T, c.res);
+        plan->launches += 4;
+        if ((e = cudaMemcpyAsync(base.data(), c.base, (kParts + 1) * 4, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    }
     plan->units.clear();
     for (u32 p = 0; p < kParts; ++p)
         for (u32 lo = base[p]; lo < base[p + 1]; lo += kUnit)
@@ -584,6 +906,7 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         const int r = v ? std::atoi(v) : 0;
         return r >= 1 && r <= (int)kMaxRounds ? (u32)r : kMaxRounds;
     }();
+    plan->launches += 1;
     const int g2 = (int)std::min<u32>(U, (u32)L.n_sm);
     k_part_agg<<<g2, kAggThreads, sm2, st>>>(c.res, c.units, U, m, max_rounds, c.dcnt, L.pkey,
                                              L.pcnt);

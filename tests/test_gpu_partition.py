@@ -37,6 +37,9 @@ elif case == "uniform_many_tiles":
     pts = np.concatenate([rng.uniform([-180, -90], [180, 90], size=(30_000_000, 2)),
                           rng.normal([10, 10], 0.01, size=(2_000_000, 2))])
     rng.shuffle(pts)
+elif case == "config5_slice_shuffled":  # a hot tile: the one-pass scatter's plan takes the exact path
+    gp = D.params(5)
+    pts = D.generate(D.spec(5, 0.05), shuffle_seed=6)  # 10M points
 elif case == "unaligned":
     gp = D.params(3)
     pts = D.generate(D.spec(3, 0.05), shuffle_seed=9)  # 5M points
@@ -86,6 +89,21 @@ def _run(case: str, **env):
 @pytest.mark.parametrize("case", ["config2_shuffled", "config4_slice_shuffled", "unaligned"])
 def test_forced_partition_path(case):
     _run(case, RG_INGEST="part")
+
+
+@pytest.mark.parametrize("scatter", ["exact", "stream"])
+@pytest.mark.parametrize("case", ["config2_shuffled", "config4_slice_shuffled",
+                                  "config5_slice_shuffled"])
+def test_both_scatters(case, scatter):
+    """KP0 + KP1 (exact histogram) and KQ0 + KQ1 (sampled plan, one pass) give
+    the oracle's counts; config 5's hot tile makes the plan fall back."""
+    _run(case, RG_INGEST="part", RG_PART=scatter)
+
+
+def test_one_pass_scatter_overflow_falls_back():
+    """Sub-regions sized below the estimate overflow; the call is redone on
+    the exact path and the counters are not double counted."""
+    _run("config2_shuffled", RG_INGEST="part", RG_PART="stream", RG_PART_SIGMA="-8")
 
 
 def test_auto_probe_picks_a_correct_path():
