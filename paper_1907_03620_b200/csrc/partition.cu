@@ -307,62 +307,91 @@ constexpr u32 kSkip = 0xffffffffu;
 // plan words (u32) after the kParts + 1 sample counters
 enum : u32 { kPlFallback = 0, kPlOverflow = 1, kPlWords = 4 };
 
-__global__ void __launch_bounds__(256) k_part_sample(const double2* xy, u64 n, Grid g, Mix m,
-                                                     u64 stride, u32* shist) {
+// Sample: groups of 8 consecutive points (one 128-byte line), one group in
+// every `frac` groups (so 1 / frac of the points), the group's place inside
+// its window hashed so a periodic input cannot alias with the stride.
+__global__ void __launch_bounds__(1024) k_part_sample(const double2* xy, u64 n, Grid g, Mix m,
+                                                     u64 frac, u32* shist) {
     __shared__ u32 hist[kParts + 1];
-    for (u32 i = threadIdx.x; i <= kParts; i += 256) hist[i] = 0;
+    for (u32 i = threadIdx.x; i <= kParts; i += 1024) hist[i] = 0;
     __syncthreads();
-    const u64 ns = (n + stride - 1) / stride;
-    for (u64 s0 = blockIdx.x * 256ull + threadIdx.x; s0 < ns; s0 += (u64)gridDim.x * 256) {
-        // offset by a per-sample hash so a periodic input cannot alias with the stride
-        const u64 i = min(n - 1, s0 * stride + ((s0 * 0x9E3779B97F4A7C15ull) >> 40) % stride);
+    const u64 n_grp = (n + 7) / 8, n_win = (n_grp + frac - 1) / frac;
+    const u32 l = threadIdx.x & 7;
+    u32 valid = 0;
+    for (u64 w = (blockIdx.x * 1024ull + threadIdx.x) >> 3; w < n_win; w += ((u64)gridDim.x * 1024) >> 3) {
+        const u64 grp = w * frac + ((w * 0x9E3779B97F4A7C15ull) >> 40) % frac;
+        const u64 i = grp * 8 + l;
         u64 k;
-        if (point_key(g, xy[i], k)) {
+        if (i < n && point_key(g, xy[i], k)) {
             atomicAdd(&hist[(u32)mix(m, k) & (kParts - 1)], 1u);
-            atomicAdd(&hist[kParts], 1u);
+            ++valid;
         }
     }
+    valid = __reduce_add_sync(kFull, valid);
+    if ((threadIdx.x & 31) == 0 && valid) atomicAdd(&hist[kParts], valid);
     __syncthreads();
-    for (u32 i = threadIdx.x; i <= kParts; i += 256)
+    for (u32 i = threadIdx.x; i <= kParts; i += 1024)
         if (hist[i]) atomicAdd(&shist[i], hist[i]);
 }
 
 // One block: capacities, region starts, fallback decision.
 //   capb[p]   entries of one block's sub-region of partition p (multiple of 8)
 //   pstart[p] first entry of partition p's region; pstart[kParts] = total
-__global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 stride, u32 nblk,
+__global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, u32 nblk,
                                                     u64 res_cap, float sigmas, u32* capb,
                                                     u32* pstart, u32* plan) {
-    __shared__ u64 tot[kParts];
+    __shared__ u64 wsum[32];
     __shared__ u32 smax;
+    static_assert(kParts == 2048, "two partitions per thread");
     if (threadIdx.x == 0) smax = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64 tot[2];
     u32 mx = 0;
-    for (u32 p = threadIdx.x; p < kParts; p += 1024) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const u32 p = 2 * threadIdx.x + q;
         const u32 sp = shist[p];
         mx = max(mx, sp);
-        const float est = (float)sp * (float)stride / (float)nblk;
-        const float sd = sqrtf(est * (1.0f + (float)stride / (float)nblk));
-        const u32 c = ((u32)(est + sigmas * sd) + 16 + 7) & ~7u;
+        const float est = (float)sp * (float)frac / (float)nblk;
+        const float sd = sqrtf(est * (1.0f + (float)frac / (float)nblk));
+        const u32 c = ((u32)fmaxf(est + sigmas * sd, 0.0f) + 16 + 7) & ~7u;
         capb[p] = c;
-        tot[p] = (u64)c * nblk;
+        tot[q] = (u64)c * nblk;
     }
-    atomicMax(&smax, mx);
+    mx = __reduce_max_sync(kFull, mx);
+    if (lane == 0) atomicMax(&smax, mx);
+    const u64 mine = tot[0] + tot[1];
+    u64 incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        u64 run = 0;
-        bool big = false;
-        for (u32 p = 0; p < kParts; ++p) {
-            pstart[p] = (u32)run;
-            run += tot[p];
-            big |= run > res_cap;
+    if (wid == 0) {
+        const u64 wv = wsum[lane];
+        u64 wi = wv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 y = __shfl_up_sync(kFull, wi, o);
+            if (lane >= o) wi += y;
         }
-        pstart[kParts] = big ? 0u : (u32)run;
-        const u64 S = shist[kParts];
-        const bool hot = (u64)smax * kQRound > (u64)kQHot * S;
-        plan[kPlFallback] = big ? 2u : (hot ? 1u : 0u);
-        plan[kPlOverflow] = 0;
+        wsum[lane] = wi - wv;
+        if (lane == 31) {
+            const bool big = wi > res_cap;
+            pstart[kParts] = big ? 0u : (u32)wi;
+            const u64 S = shist[kParts];
+            const bool hot = (u64)smax * kQRound > (u64)kQHot * S;
+            plan[kPlFallback] = big ? 2u : (hot ? 1u : 0u);
+            plan[kPlOverflow] = 0;
+        }
     }
+    __syncthreads();
+    const u64 ex = wsum[wid] + incl - mine;  // (wraps harmlessly when the plan falls back)
+    pstart[2 * threadIdx.x] = (u32)ex;
+    pstart[2 * threadIdx.x + 1] = (u32)(ex + tot[0]);
 }
 
 struct StreamArgs {
@@ -386,12 +415,26 @@ __device__ __forceinline__ u64 stream_key(const Grid& g, double2 v) {
     return pack_key(g, v.x, v.y);
 }
 
+__device__ __forceinline__ u32 sh_atom_inc(u32 addr) {
+    u32 old;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(addr) : "memory");
+    return old;
+}
+__device__ __forceinline__ void sh_st(u32 addr, u32 v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 sh_ld(u32 addr) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 template <bool kNarrow>
 __global__ void __launch_bounds__(kQThr, 1) k_part_stream(StreamArgs A) {
     extern __shared__ u32 sh_q[];
-    u32* buf = sh_q;                    // kParts x kQC residuals
-    u32* cnt = buf + kParts * kQC;      // entries waiting per partition
-    u32* bcur = cnt + kParts;           // next entry of this block's sub-region
+    u32* buf = sh_q;                    // kParts x kQC residuals: a ring per partition
+    u32* cw = buf + kParts * kQC;       // entries waiting | ring head << 16 (head: 0, 8 or 16)
+    u32* bcur = cw + kParts;            // next entry of this block's sub-region
     u32* bend = bcur + kParts;          // end of this block's sub-region
     u32* list = bend + kParts;          // partitions with a full sector this round
     __shared__ u32 nlist;
@@ -399,50 +442,81 @@ __global__ void __launch_bounds__(kQThr, 1) k_part_stream(StreamArgs A) {
     const u32 tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const u32 nblk = gridDim.x, b = blockIdx.x;
     for (u32 p = tid; p < kParts; p += kQThr) {
-        cnt[p] = 0;
+        cw[p] = 0;
         bcur[p] = A.pstart[p] + b * A.capb[p];
         bend[p] = A.pstart[p] + (b + 1) * A.capb[p];
     }
     if (tid == 0) nlist = 0;
+    u32 s_buf = (u32)__cvta_generic_to_shared(buf);
+    u32 s_cw = (u32)__cvta_generic_to_shared(cw);
+    // (opaque to the compiler: it would otherwise recompute the window
+    // addresses at every use instead of keeping two registers)
+    asm volatile("" : "+r"(s_buf), "+r"(s_cw));
     const u64 pol = evict_first_policy();
     const double2 nanpt = make_double2(__longlong_as_double(0x7ff8000000000000ll), 0.0);
     const u64 n = A.n, n_rounds = (n + kQRound - 1) / kQRound;
     const Grid g = A.g;
     const Mix m = A.m;
-    u64 in = 0, seen = 0;
-    bool over = false;
+    u32* const res = A.res;
+    u32 in = 0, seen = 0;  // per thread: fewer than 2^31 points in all
+    u32 over = 0;
     double2 v[kQPer];
+    // points of round r this thread owns: those j with j * kQThr < avail(r)
+    auto avail = [&](u64 r) -> u32 {
+        const u64 base = r * kQRound + tid;
+        return r < n_rounds && n > base ? (u32)min(n - base, (u64)kQRound) : 0u;
+    };
+    {
+        const u32 av = avail(b);
+        const double2* src = A.xy + (u64)b * kQRound + tid;
 #pragma unroll
-    for (int j = 0; j < kQPer; ++j) {
-        const u64 i = (u64)b * kQRound + (u64)j * kQThr + tid;
-        v[j] = (b < n_rounds && i < n) ? ld_point_stream(A.xy + i, pol) : nanpt;
+        for (int j = 0; j < kQPer; ++j)
+            v[j] = (u32)j * kQThr < av ? ld_point_stream(src + j * kQThr, pol) : nanpt;
     }
     __syncthreads();
+    u32 av = avail(b);
     for (u64 r = b; r < n_rounds; r += nblk) {
-        const u64 nx = r + nblk;
-        {
-            const u64 base = r * kQRound + tid;
-            const u64 left = n > base ? n - base : 0;  // points j with j * kQThr < left exist
-            seen += min((u64)kQPer, (left + kQThr - 1) / kQThr);
-        }
+        seen += (av + kQThr - 1) / kQThr;
+        // Keys of the round's points (branch-free: an out-of-bounds point's
+        // key is computed and dropped), while the next round's loads are
+        // issued into the registers the points leave.
+        av = avail(r + nblk);
+        const double2* src = A.xy + (r + nblk) * kQRound + tid;
+#ifndef RG_KQ_G
+#define RG_KQ_G 1
+#endif
+        constexpr int kG = RG_KQ_G;  // points whose shared-memory atomics are in flight together
 #pragma unroll
-        for (int j = 0; j < kQPer; ++j) {
-            const double2 pt = v[j];
-            const u64 i = nx * kQRound + (u64)j * kQThr + tid;
-            v[j] = (nx < n_rounds && i < n) ? ld_point_stream(A.xy + i, pol) : nanpt;
-            if (in_bounds(g, pt.x, pt.y)) {
+        for (int j0 = 0; j0 < kQPer; j0 += kG) {
+            u32 part[kG], rr[kG], old[kG];
+            u32 vmask = 0;
+#pragma unroll
+            for (int j = 0; j < kG; ++j) {
+                const double2 pt = v[j0 + j];
+                v[j0 + j] = (u32)(j0 + j) * kQThr < av ? ld_point_stream(src + (j0 + j) * kQThr, pol) : nanpt;
                 const u64 h = mix(m, stream_key<kNarrow>(g, pt));
-                const u32 p = (u32)h & (kParts - 1);
-                const u32 rr = (u32)(h >> kPBits);
-                const u32 rank = atomicAdd(&cnt[p], 1u);
-                if (rank < kQC) {
-                    buf[p * kQC + rank] = rr;
-                } else {  // buffer full (rare): straight to the sub-region
-                    const u32 at = atomicAdd(&bcur[p], 1u);
-                    if (at < bend[p]) A.res[at] = rr;
-                    else over = true;
+                part[j] = (u32)h & (kParts - 1);
+                rr[j] = (u32)(h >> kPBits);
+                vmask |= in_bounds(g, pt.x, pt.y) ? 1u << j : 0u;
+            }
+            in += __popc(vmask);
+#pragma unroll
+            for (int j = 0; j < kG; ++j)
+                if (vmask >> j & 1) old[j] = sh_atom_inc(s_cw + part[j] * 4);
+#pragma unroll
+            for (int j = 0; j < kG; ++j) {
+                if (vmask >> j & 1) {
+                    const u32 rank = old[j] & 0xffffu;
+                    if (rank < kQC) {
+                        u32 pos = (old[j] >> 16) + rank;
+                        pos = pos >= kQC ? pos - kQC : pos;
+                        sh_st(s_buf + (part[j] * kQC + pos) * 4, rr[j]);
+                    } else {  // buffer full (rare): straight to the sub-region
+                        const u32 at = atomicAdd(&bcur[part[j]], 1u);
+                        if (at < bend[part[j]]) res[at] = rr[j];
+                        else over = 1;
+                    }
                 }
-                ++in;
             }
         }
         __syncthreads();
@@ -450,34 +524,40 @@ __global__ void __launch_bounds__(kQThr, 1) k_part_stream(StreamArgs A) {
 #pragma unroll
         for (int q = 0; q < (int)(kParts / kQThr); ++q) {
             const u32 p = q * kQThr + tid;
-            const u32 c = cnt[p];
-            if (c > kQC) cnt[p] = kQC;
-            const u32 msk = __ballot_sync(kFull, c >= 8);
+            const u32 w = cw[p];
+            if ((w & 0xffffu) > kQC) cw[p] = (w & 0xffff0000u) | kQC;
+            const bool fl = (w & 0xffffu) >= 8;
+            const u32 msk = __ballot_sync(kFull, fl);
             u32 at = 0;
             if (lane == 0 && msk) at = atomicAdd(&nlist, (u32)__popc(msk));
             at = __shfl_sync(kFull, at, 0);
-            if (c >= 8) list[at + __popc(msk & ((1u << lane) - 1))] = p;
+            if (fl) list[at + __popc(msk & ((1u << lane) - 1))] = p;
         }
         __syncthreads();
         {
-            const u32 nl = nlist, l = lane & 7, grp = lane >> 3;
-            for (u32 e0 = wid * 4; e0 < nl; e0 += (kQThr / 32) * 4) {
-                const u32 e = e0 + grp;
-                if (e < nl) {
-                    const u32 p = list[e];
-                    const u32 c = cnt[p], nfl = c & ~7u, base = bcur[p];
-                    const bool ok = base + nfl <= bend[p];
-                    if (ok)
-                        for (u32 j = 0; j < nfl; j += 8) A.res[base + j + l] = buf[p * kQC + j + l];
-                    else
-                        over = true;
-                    // the tail (< 8 entries, beyond the flushed part) moves to the front
-                    if (l < c - nfl) buf[p * kQC + l] = buf[p * kQC + nfl + l];
-                    if (l == 0) {
-                        cnt[p] = c - nfl;
-                        if (ok) bcur[p] = base + nfl;
-                    }
+            // a group of 8 lanes writes a partition's full sectors (at most
+            // three) and retires them from the ring
+            const u32 nl = nlist, l = lane & 7;
+            for (u32 e = tid >> 3; e < nl; e += kQThr / 8) {
+                const u32 p = list[e];
+                const u32 w = cw[p], c = w & 0xffffu, h = w >> 16, base = bcur[p];
+                const u32 nsec = c >> 3;  // 1..3
+                u32 h1 = h + 8, h2 = h + 16, h3 = h + 24;
+                h1 -= h1 >= kQC ? kQC : 0;
+                h2 -= h2 >= kQC ? kQC : 0;
+                h3 -= h3 >= kQC ? kQC : 0;
+                const u32 sb = s_buf + (p * kQC + l) * 4;
+                if (base + 8 * nsec <= bend[p]) {
+                    u32* dst = res + (base + l);
+                    dst[0] = sh_ld(sb + h * 4);
+                    if (nsec > 1) dst[8] = sh_ld(sb + h1 * 4);
+                    if (nsec > 2) dst[16] = sh_ld(sb + h2 * 4);
+                    if (l == 0) bcur[p] = base + 8 * nsec;
+                } else {
+                    over = 1;
                 }
+                const u32 hn = nsec == 1 ? h1 : (nsec == 2 ? h2 : h3);
+                if (l == 0) cw[p] = (c & 7u) | (hn << 16);
             }
         }
         if (tid == 0) nlist = 0;
@@ -485,19 +565,22 @@ __global__ void __launch_bounds__(kQThr, 1) k_part_stream(StreamArgs A) {
     }
     // tails, then the skip marker through the end of every sub-region
     for (u32 p = wid; p < kParts; p += kQThr / 32) {
-        const u32 c = min(cnt[p], kQC), base = bcur[p];
+        const u32 w = cw[p], c = min(w & 0xffffu, kQC), h = w >> 16, base = bcur[p];
         const u32 end = bend[p];
-        if (base + c > end) over = true;
-        for (u32 i = lane; base + i < end; i += 32) A.res[base + i] = i < c ? buf[p * kQC + i] : kSkip;
+        if (base + c > end) over = 1;
+        for (u32 i = lane; base + i < end; i += 32) {
+            const u32 pos = h + i >= kQC ? h + i - kQC : h + i;
+            res[base + i] = i < c ? buf[p * kQC + pos] : kSkip;
+        }
     }
-    if (__any_sync(kFull, over) && lane == 0) A.plan[kPlOverflow] = 1;
-    u64 out = seen - in;
+    if (__any_sync(kFull, over != 0) && lane == 0) A.plan[kPlOverflow] = 1;
+    u64 in64 = in, out = seen - in;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        in += __shfl_xor_sync(kFull, in, o);
+        in64 += __shfl_xor_sync(kFull, in64, o);
         out += __shfl_xor_sync(kFull, out, o);
     }
-    if (lane == 0 && in) atomicAdd(&A.inout[0], in);
+    if (lane == 0 && in64) atomicAdd(&A.inout[0], in64);
     if (lane == 0 && out) atomicAdd(&A.inout[1], out);
 }
 
@@ -828,12 +911,12 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         // one-pass scatter: sample, plan, stream
         const u64 n_rounds = (n + kQRound - 1) / kQRound;
         const u32 nblk = (u32)std::min<u64>((u64)L.n_sm, std::max<u64>(1, n_rounds / 8));
-        const u64 stride = std::min<u64>(128, std::max<u64>(1, n >> 18));
+        const u64 stride = std::min<u64>(128, std::max<u64>(1, n >> 18));  // 1 / stride of the points
         const u64 res_cap = std::min<u64>(partition_res_entries(n), 0xfffffff0ull);
         if ((e = cudaMemsetAsync(c.shist, 0, (kParts + 1 + kPlWords) * 4, st)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(c.inout, 0, 16, st)) != cudaSuccess) return e;
-        const u64 ns = (n + stride - 1) / stride;
-        k_part_sample<<<(int)std::min<u64>((ns + 255) / 256, (u64)L.n_sm * 8), 256, 0, st>>>(
+        const u64 n_win = ((n + 7) / 8 + stride - 1) / stride;
+        k_part_sample<<<(int)std::min<u64>((n_win * 8 + 1023) / 1024, (u64)L.n_sm * 2), 1024, 0, st>>>(
             xy, n, L.g, m, stride, c.shist);
         k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, nblk, res_cap, sigmas, c.capb, c.pstart,
                                         c.plan);
