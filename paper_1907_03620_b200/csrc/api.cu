@@ -365,6 +365,17 @@ struct rg_ctx {
     u32* pair_cnt = nullptr;
     u64 pair_cap = 0;
     int part_stream_hint = 0;  // 1: the one-pass scatter fell back for the probed buffer
+    // K2 from the partitioned contraction's pairs (rg_cluster of one device
+    // span into an empty table): the pairs are final counts, so prune filters
+    // them while their insertion into the table (KP3) runs on aux_st.
+    bool allow_pairs_k2 = false;   // set by rg_cluster_ex around its ingest
+    bool pairs_k2 = false;         // the pair slabs below describe the whole accumulator
+    const uint4* pk_units = nullptr;
+    const u32* pk_dcnt = nullptr;
+    u32 pk_n_units = 0;
+    bool insert_pending = false;   // KP3 in flight on aux_st (ev_kp3)
+    cudaEvent_t ev_kp3 = nullptr;
+    bool slot_of_valid = true;     // K2 recorded the table slots of the significant tiles
     u64 order_probe[3] = {0, 0, 0};
     u64 probe_fp = 0;       // fingerprint of the probed buffer's content
     u64* k2_lb = nullptr;   // K2's look-back status words
@@ -750,6 +761,18 @@ bool buffer_unordered(rg_ctx* ctx, const double* xy, u64 n) {
     return ctx->probe_unordered;
 }
 
+bool dedupe_active(const rg_ctx* ctx);
+
+// The table is complete again once the main stream has waited for a KP3
+// that was left running on aux_st.
+rg_status settle_insert(rg_ctx* ctx) {
+    if (ctx->insert_pending) {
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_kp3, 0));
+        ctx->insert_pending = false;
+    }
+    return RG_OK;
+}
+
 rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
     size_t scan_temp = 0;
     const size_t need = partition_scratch_bytes(n, &scan_temp);
@@ -772,6 +795,8 @@ rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
     }
     PartitionPlan plan;
     PhaseTimer timer(ctx, &ctx->ms_contract);
+    const u64 used_before = ctx->used;
+    ctx->pairs_k2 = false;
     PartitionLaunch L;
     L.xy = xy;
     L.n = n;
@@ -794,6 +819,35 @@ rg_status ingest_partitioned(rg_ctx* ctx, const double* xy, u64 n) {
     while ((double)(ctx->used + pairs + plan.raw_points) >= kMaxLoad * (double)ctx->cap) {
         rg_status s = grow_table(ctx, ctx->cap * 2);
         if (s != RG_OK) return s;
+    }
+    // rg_cluster of one device span into an empty table, every partition one
+    // work unit: the pairs are the final counts. K2 then filters the pairs
+    // (prune_enqueue) and KP3 fills the table on aux_st beside K2 and K3.
+    static const bool pairs_off = [] {
+        const char* v = std::getenv("RG_PAIRS_K2");
+        return v && std::strcmp(v, "0") == 0;
+    }();
+    const bool defer = ctx->allow_pairs_k2 && !pairs_off && used_before == 0 && pairs > 0 &&
+                       plan.raw_points == 0 && plan.single_units && !dedupe_active(ctx);
+    if (defer) {
+        CK(cudaEventRecord(ctx->ev_kp3, ctx->st));
+        CK(cudaStreamWaitEvent(ctx->aux_st, ctx->ev_kp3, 0));
+        static const int side_bps = [] {
+            const char* v = std::getenv("RG_KP3_SIDE_BPS");
+            const int b = v ? std::atoi(v) : 0;
+            return b >= 1 && b <= 64 ? b : 16;
+        }();
+        CK(launch_partition_insert(L, table_of(ctx), plan, ctx->aux_st, side_bps));
+        CK(cudaEventRecord(ctx->ev_kp3, ctx->aux_st));
+        ctx->launches += 1;
+        ctx->insert_pending = true;
+        ctx->pairs_k2 = true;
+        ctx->pk_units = plan.units_dev;
+        ctx->pk_dcnt = plan.dcnt_dev;
+        ctx->pk_n_units = (u32)plan.units.size();
+        rg_status s = pull_counters(ctx);  // ingested / skipped (KP3 is still adding to `used`)
+        ctx->used = pairs;                 // one claim per pair into the empty table
+        return s;
     }
     CK(launch_partition_insert(L, table_of(ctx), plan, ctx->st));
     ctx->launches += 1 + (plan.raw_points ? 1 : 0);
@@ -1202,6 +1256,14 @@ rg_status mark_table(rg_ctx* ctx, bool with_cids) {
         rg_status s = ensure_tile_cid(ctx);
         if (s != RG_OK) return s;
     }
+    if (!ctx->slot_of_valid) {  // K2 ran on the pairs: look the slots up
+        rg_status si = settle_insert(ctx);
+        if (si != RG_OK) return si;
+        CK(launch_find_slots(table_of(ctx), ctx->sig_key, ctx->n_sig, ctx->slot_of, ctx->n_sm,
+                             ctx->st));
+        ++ctx->launches;
+        ctx->slot_of_valid = true;
+    }
     CK(launch_mark_sig(table_of(ctx), ctx->slot_of, with_cids ? ctx->tile_cid : nullptr,
                        ctx->n_sig, ctx->n_sm, ctx->st));
     ++ctx->launches;
@@ -1225,6 +1287,15 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
     if (s != RG_OK) return s;
     zero_field(ctx, &ctx->ctr->n_sig);
     ctx->tile_cid_pending = false;
+    // the pairs of a partitioned contraction stand in for the table scan
+    // (consumed here: any later change of the table invalidates them)
+    const bool from_pairs = ctx->pairs_k2 && ctx->slots && used && use_sorted_k3(ctx) &&
+                            !window_fix && !(dedupe_active(ctx) && ctx->ut);
+    ctx->pairs_k2 = false;
+    if (!from_pairs) {  // everything below reads the table: a KP3 in flight must land first
+        rg_status si = settle_insert(ctx);
+        if (si != RG_OK) return si;
+    }
     if (ctx->slots && used) {
         const bool hash_k3 = !use_sorted_k3(ctx);
         if (window_fix) {
@@ -1257,12 +1328,21 @@ rg_status prune_enqueue(rg_ctx* ctx, bool window_fix) {
             CK(dalloc(&ctx->k2_lb, compact_lb_words(ctx->cap)));
             ctx->k2_lb_words = compact_lb_words(ctx->cap);
         }
-        CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
-                          window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
-                          ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts, ctx->min_key,
-                          ctx->root_cid, cols ? ctx->s_col_cnt : nullptr,
-                          hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st,
-                          ctx->k2_lb));
+        if (from_pairs) {
+            CK(launch_compact_pairs(ctx->pk_units, ctx->pk_dcnt, ctx->pk_n_units, ctx->pair_key,
+                                    ctx->pair_cnt, ctx->p.threshold, ctx->sig_key, ctx->sig_cnt,
+                                    cols ? ctx->s_col_cnt : nullptr, ctx->grid.bits_y, ctx->ctr,
+                                    ctx->n_sm, ctx->st));
+            ctx->slot_of_valid = false;  // looked up if SIG marks are ever needed (mark_table)
+        } else {
+            CK(launch_compact(table_of(ctx), ctx->cap, ctx->p.threshold,
+                              window_fix ? ctx->wf_keep : nullptr, ctx->sig_key, ctx->sig_cnt,
+                              ctx->parent, hash_k3 ? ctx->size : nullptr, ctx->npts,
+                              ctx->min_key, ctx->root_cid, cols ? ctx->s_col_cnt : nullptr,
+                              hash_k3 ? nullptr : ctx->slot_of, ctx->ctr, ctx->n_sm, ctx->st,
+                              ctx->k2_lb));
+            ctx->slot_of_valid = true;
+        }
         ++ctx->launches;
         ctx->col_hist_ready = cols != 0;
         if (ctx->alt_dirty && ctx->slots_alt && ctx->cap_alt == ctx->cap) {
@@ -1625,8 +1705,15 @@ rg_status rg_create(const rg_params* p, int device, rg_ctx** out) {
     ctx->st = ctx->own;
     if ((e = cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking)) != cudaSuccess)
         return fail(e, "stream");
-    if ((e = cudaStreamCreateWithFlags(&ctx->aux_st, cudaStreamNonBlocking)) != cudaSuccess)
-        return fail(e, "stream");
+    {
+        // side work (the idle table's clear, a deferred KP3) yields to the main stream
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&ctx->aux_st, cudaStreamNonBlocking, lo)) != cudaSuccess)
+            return fail(e, "stream");
+    }
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_kp3, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(e, "event");
     if ((e = cudaEventCreateWithFlags(&ctx->ev_alt, cudaEventDisableTiming)) != cudaSuccess)
         return fail(e, "event");
     if ((e = cudaEventCreate(&ctx->t0)) != cudaSuccess) return fail(e, "event");
@@ -1728,6 +1815,7 @@ void rg_destroy(rg_ctx* ctx) {
     if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
     if (ctx->t1) cudaEventDestroy(ctx->t1);
     if (ctx->ev_alt) cudaEventDestroy(ctx->ev_alt);
+    if (ctx->ev_kp3) cudaEventDestroy(ctx->ev_kp3);
     if (ctx->aux_st) cudaStreamDestroy(ctx->aux_st);
     if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -1868,6 +1956,11 @@ rg_status rg_stream_end(rg_ctx* ctx) {
 // Any other call on a context with an open stream closes it first (its
 // counters and table must be final).
 static rg_status settle_stream(rg_ctx* ctx) {
+    if (ctx->insert_pending) {  // (only after an error between ingest and prune)
+        DevGuard guard(ctx->device);
+        const rg_status si = settle_insert(ctx);
+        if (si != RG_OK) return si;
+    }
     return ctx->streaming ? rg_stream_end(ctx) : RG_OK;
 }
 
@@ -2422,6 +2515,10 @@ rg_status prune_agglomerate_fused(rg_ctx* ctx, bool window_fix) {
         zero_field(ctx, &ctx->ctr->n_kept);
     }
     CK(cudaEventRecord(ctx->ev_end, ctx->st));
+    {  // the table is complete when the call returns
+        rg_status si = settle_insert(ctx);
+        if (si != RG_OK) return si;
+    }
     CK(cudaMemcpyAsync(ctx->hctr, ctx->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     check_fingerprint(ctx);
@@ -2489,7 +2586,10 @@ rg_status rg_cluster_ex(rg_ctx* ctx, const double* xy, uint64_t n, rg_memkind ki
     if (s != RG_OK) return s;
     const bool sorted_k3 = use_sorted_k3(ctx);
     // with the sorted K3 the K1 stop check rides on K3's host read
+    const bool wf_req = (flags & RG_CLUSTER_WINDOW_FIX) != 0;
+    ctx->allow_pairs_k2 = sorted_k3 && !wf_req && kind == RG_MEM_DEVICE;
     s = ingest_any(ctx, xy, n, kind, sorted_k3 && n < 0x7fffffffull);
+    ctx->allow_pairs_k2 = false;
     if (s != RG_OK) return s;
     u64 peak = ctx->used;
     const bool wf = (flags & RG_CLUSTER_WINDOW_FIX) != 0;

@@ -230,6 +230,12 @@ __device__ __forceinline__ bool table_add_cas128(const Table& t, u64 key, u64 cn
     }
 }
 
+// L2 prefetch of a key's home slot (no register result: fire and forget).
+__device__ __forceinline__ void prefetch_slot(const Table& t, u64 key) {
+    const Probe p(key, t);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(t.slots + p.slot()));
+}
+
 // Lookup: returns the slot's value word, or kEmpty when the key is absent.
 // TileCounts::count_of accumulator.hpp:53-61.
 __device__ __forceinline__ u64 table_find(const Table& t, u64 key) {

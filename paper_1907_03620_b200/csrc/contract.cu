@@ -135,7 +135,7 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
 // with count 0; then every missing lane whose key now owns its slot adds
 // 1, and the others (a different key won the slot in this row) stage
 // (key, 1) themselves.
-template <bool kNarrow>
+template <bool kNarrow, bool kPf>
 __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
                                               int lane, u32 lt_mask, u32 budget) {
@@ -205,7 +205,7 @@ __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, con
 // placeholder if the slot was empty) and installs its key with count 0;
 // every missing point whose key now owns its slot adds 1, the others stage
 // (key, 1). Each winner and each loser adds one staged entry.
-template <bool kNarrow>
+template <bool kNarrow, bool kPf>
 __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
                                               int lane, u32 lt_mask, u32 budget) {
@@ -247,6 +247,13 @@ __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, con
             sc[r] = w.ccnt[cs[r]];
             w.ckey[cs[r]] = key[r];
             w.ccnt[cs[r]] = 0;
+            // The evicted tile waits in the staging list for the next flush
+            // (at most 64 entries away). For tables up to 256 MB its home
+            // slot's sector is fetched into L2 now, so the flush's CAS does
+            // not wait on DRAM (config 3: K1 0.354 -> 0.320 ms); with config
+            // 4's 537 MB table the same prefetch costs 8 % (1.56 -> 1.68 ms),
+            // as does prefetching when a tile enters the cache.
+            if (kPf && sk[r] != kEmpty) prefetch_slot(t, sk[r]);
         }
     }
     __syncwarp();
@@ -337,7 +344,7 @@ constexpr int kK1Unroll = RG_K1_UNROLL;  // batches per trip of run_segment's lo
 // into its own ring column, so no cross-lane synchronisation is needed
 // around the ring. Returns the row index at which the warp ran out of
 // budget, or nr.
-template <bool kAligned, bool kNarrow, bool kFullRows>
+template <bool kAligned, bool kNarrow, bool kFullRows, bool kPf>
 __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy_base, u32 nr,
                                            u32 valid, double2 (*ring)[32], const Grid& g,
                                            const Table& t, WarpSmem& w, K1State& st, int lane,
@@ -381,7 +388,7 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
         for (int b = 0; b < kBatch; ++b) st.added += (x[b] + y[b] > 1e300) ? 1 : 0;
         const bool over = false;
 #else
-        const bool over = process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask, budget);
+        const bool over = process_batch<kNarrow, kPf>(g, t, x, y, w, st, lane, lt_mask, budget);
 #endif
         if (over) return j + kBatch < nr ? j + kBatch : nr;
     }
@@ -393,7 +400,7 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
 // once every lane has read it. `phase` carries the stages' mbarrier parities
 // across segments. Same return convention as run_segment.
 constexpr int kStages = kRing / kBatch;
-template <bool kNarrow>
+template <bool kNarrow, bool kPf>
 __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 valid,
                                                double2 (*ring)[32], u64* bar, u32& phase,
                                                const Grid& g, const Table& t, WarpSmem& w,
@@ -427,7 +434,7 @@ __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 v
 #endif
             issue(b + kStages);
         }
-        if (process_batch<kNarrow>(g, t, x, y, w, st, lane, lt_mask, budget)) {
+        if (process_batch<kNarrow, kPf>(g, t, x, y, w, st, lane, lt_mask, budget)) {
             done_b = b + 1;
             break;
         }
@@ -441,7 +448,7 @@ __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 v
     return done_b < nb ? done_b * kBatch : nr;
 }
 
-template <bool kAligned, bool kNarrow, bool kTma>
+template <bool kAligned, bool kNarrow, bool kTma, bool kPf = false>
 __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ WarpSmem s_warp[kWarpsPerBlock];
     __shared__ __align__(16) double2 s_ring[kWarpsPerBlock][kRing][32];
@@ -538,13 +545,13 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         const double* xy_base = P.xy + 2 * p0;
         u32 done;
         if (kTma)
-            done = run_segment_tma<kNarrow>(pts + p0, nr, valid, ring, bar, phase, g, t, w, st,
+            done = run_segment_tma<kNarrow, kPf>(pts + p0, nr, valid, ring, bar, phase, g, t, w, st,
                                             lane, lt_mask, pol, P.budget);
         else if (valid == nr * 32 && nr % kBatch == 0)
-            done = run_segment<kAligned, kNarrow, true>(base, xy_base, nr, valid, ring, g, t, w,
+            done = run_segment<kAligned, kNarrow, true, kPf>(base, xy_base, nr, valid, ring, g, t, w,
                                                         st, lane, lt_mask, pol, P.budget);
         else
-            done = run_segment<kAligned, kNarrow, false>(base, xy_base, nr, valid, ring, g, t, w,
+            done = run_segment<kAligned, kNarrow, false, kPf>(base, xy_base, nr, valid, ring, g, t, w,
                                                          st, lane, lt_mask, pol, P.budget);
         if (!kTma) cp_async_wait<0>();
         n_valid += min((u64)done * 32, (u64)valid);
@@ -939,6 +946,103 @@ __global__ void __launch_bounds__(kK2LbThr) k_compact_lb(Table t, u64 cap, u64 t
     }
 }
 
+// K2 over (key, count) pairs instead of the table: after a partitioned
+// contraction into an empty table every work unit's pairs are final counts
+// (one unit per partition), so prune (accumulator.hpp:160-174) is a filter
+// of the pair slabs - 150 MB for config 4 instead of the 537 MB table -
+// and does not wait for the pairs' insertion into the table, which runs
+// beside K2 and K3 on another stream. One block per unit; a reservation
+// atomic per 1024 pairs; the column histogram as in k_compact_lb. The
+// table slots of the significant tiles are not known here (k_find_slots
+// looks them up if SIG marks are ever needed).
+__global__ void __launch_bounds__(256) k_compact_pairs(const uint4* units, const u32* dcnt,
+                                                       u32 n_units, const u64* pkey,
+                                                       const u32* pcnt, u64 tau, K2Out o,
+                                                       Counters* ctr) {
+    __shared__ u32 s_warp[33];
+    __shared__ u64 s_pre;
+    const int lane = threadIdx.x & 31;
+    constexpr int kPer = 4;
+    for (u32 u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const u64 lo = units[u].x;
+        const u32 d = dcnt[u];
+        for (u32 i0 = 0; i0 < d; i0 += 256 * kPer) {
+            u64 k[kPer];
+            u32 v[kPer];
+            u32 flags = 0;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const u32 i = i0 + j * 256 + threadIdx.x;
+                k[j] = kEmpty;
+                v[j] = 0;
+                if (i < d) {
+                    k[j] = pkey[lo + i];
+                    v[j] = pcnt[lo + i];
+                }
+                flags |= (u32)(i < d && v[j] >= tau) << j;
+            }
+            u32 agg;
+            const u32 ex = block_excl_sum<256>((u32)__popc(flags), s_warp, &agg);
+            if (threadIdx.x == 0) s_pre = agg ? atomicAdd(&ctr->n_sig, (u64)agg) : 0;
+            __syncthreads();
+            u64 pos = s_pre + ex;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const bool sig = (flags >> j) & 1u;
+                if (sig) {
+                    o.sig_key[pos] = k[j];
+                    o.sig_cnt[pos] = v[j];
+                    ++pos;
+                }
+                if (o.col_cnt) {
+                    const u32 col = sig ? (u32)(k[j] >> o.bits_y) : 0xffffffffu;
+                    const u32 peers = __match_any_sync(kFull, col);
+                    if (sig && lane == __ffs(peers) - 1)
+                        red_add_u32(o.col_cnt + col, (u32)__popc(peers));
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Table slot of every significant tile (for the SIG marks, after a K2 that
+// did not scan the table).
+__global__ void k_find_slots(Table t, const u64* sig_key, u64 n, u32* slot_of) {
+    for (u64 pos = blockIdx.x * (u64)blockDim.x + threadIdx.x; pos < n;
+         pos += (u64)gridDim.x * blockDim.x) {
+        const u64 key = sig_key[pos];
+        Probe p(key, t);
+        while (true) {
+            const u64 k = ld_key(t.slots + p.slot());
+            if (k == key || k == kEmpty) break;  // (every significant tile is in the table)
+            p.next(t);
+        }
+        slot_of[pos] = (u32)p.slot();
+    }
+}
+
+cudaError_t launch_compact_pairs(const uint4* units, const u32* dcnt, u32 n_units, const u64* pkey,
+                                 const u32* pcnt, u64 tau, u64* sig_key, u64* sig_cnt,
+                                 u32* col_cnt, u32 bits_y, Counters* ctr, int n_sm,
+                                 cudaStream_t st) {
+    if (n_units == 0) return cudaSuccess;
+    const K2Out o{sig_key, sig_cnt, nullptr, nullptr, nullptr, nullptr, nullptr, col_cnt, bits_y,
+                  nullptr};
+    const u32 blocks = n_units < (u32)n_sm * 16 ? n_units : (u32)n_sm * 16;
+    k_compact_pairs<<<(int)blocks, 256, 0, st>>>(units, dcnt, n_units, pkey, pcnt, tau, o, ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_find_slots(Table t, const u64* sig_key, u64 n, u32* slot_of, int n_sm,
+                              cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const u64 want = (n + 255) / 256;
+    const int blocks = (int)(want < (u64)n_sm * 16 ? want : (u64)n_sm * 16);
+    k_find_slots<<<blocks, 256, 0, st>>>(t, sig_key, n, slot_of);
+    return cudaGetLastError();
+}
+
 // Deferred SIG marks (sorted K3 path): the count word of significant tile
 // pos becomes SIG | pos (dense index, as K2 writes it on the hash path) or
 // SIG | (cluster id + 1) (K4's lookups then need no second load).
@@ -966,14 +1070,15 @@ static int g_k1_warps_per_sm = 0;
 // overshoot its load target (see ingest_device in api.cu).
 int contract_max_warps(int n_sm) {
     if (!g_k1_warps_per_sm) {
-        int b[5] = {0, 0, 0, 0, 0};
+        int b[6] = {0, 0, 0, 0, 0, 0};
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_contract<true, true, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_contract<true, false, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_contract<false, true, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_contract<false, false, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[4], k_contract<true, true, true>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[5], k_contract<true, true, false, true>, kThreads, 0);
         int m = b[0];
-        for (int i = 1; i < 5; ++i) m = b[i] < m ? b[i] : m;
+        for (int i = 1; i < 6; ++i) m = b[i] < m ? b[i] : m;
         g_k1_warps_per_sm = (m < 1 ? 1 : m) * kWarpsPerBlock;
     }
     return g_k1_warps_per_sm * n_sm;
@@ -996,6 +1101,12 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     P.n_partial_in = L.n_partial_in;
     P.partial_out = L.partial_out;
     P.budget = (u32)(L.budget < (1ull << 30) ? L.budget : (1ull << 30));
+    static const int pf_mode = [] {  // RG_K1_PREFETCH=0 / =1 forces it (A/B)
+        const char* v = std::getenv("RG_K1_PREFETCH");
+        return v ? (std::strcmp(v, "0") == 0 ? 0 : 1) : -1;
+    }();
+    const u64 table_bytes = (L.t.bmask + 1) * kBucketSlots * sizeof(Slot);
+    const bool prefetch = pf_mode >= 0 ? pf_mode != 0 : table_bytes <= (256ull << 20);
     const int blocks = (int)((L.warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const bool aligned = ((uintptr_t)L.xy & 15) == 0;
     // RG_K1=tma selects the TMA bulk-copy ring (measured slower than the
@@ -1006,6 +1117,8 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     }();
     if (aligned && L.narrow && tma)
         k_contract<true, true, true><<<blocks, kThreads, 0, st>>>(P);
+    else if (aligned && L.narrow && prefetch)
+        k_contract<true, true, false, true><<<blocks, kThreads, 0, st>>>(P);
     else if (aligned && L.narrow)
         k_contract<true, true, false><<<blocks, kThreads, 0, st>>>(P);
     else if (aligned)

@@ -40,6 +40,12 @@ cudaError_t launch_first_oob(const double* xy, u64 n, Grid g, u64* first, int n_
 // lb_scratch (K2 look-back: cap / 2048 + 2 words) selects the one-pass K2;
 // null selects the staged K2 (reservation atomics)
 u64 compact_lb_words(u64 cap);
+cudaError_t launch_compact_pairs(const uint4* units, const u32* dcnt, u32 n_units, const u64* pkey,
+                                 const u32* pcnt, u64 tau, u64* sig_key, u64* sig_cnt,
+                                 u32* col_cnt, u32 bits_y, Counters* ctr, int n_sm,
+                                 cudaStream_t st);
+cudaError_t launch_find_slots(Table t, const u64* sig_key, u64 n, u32* slot_of, int n_sm,
+                              cudaStream_t st);
 cudaError_t launch_compact(Table t, u64 cap, u64 tau, const u8* keep, u64* sig_key, u64* sig_cnt,
                            u32* parent, u32* size, u64* npts, u64* min_key, int* root_cid,
                            u32* col_cnt, u32* slot_of, Counters* ctr, int n_sm,
@@ -169,10 +175,13 @@ struct PartitionPlan {
                                 // (pairs live in per-unit slabs at units[u].x)
     u64 raw_points = 0;         // points of overflowed units (added one by one)
     int launches = 0;           // kernels launched by launch_partition_count
+    bool single_units = true;   // every partition is one work unit (its pairs are final counts)
+    const uint4* units_dev = nullptr;  // device copies of units / dcnt (in the scratch)
+    const u32* dcnt_dev = nullptr;
 };
 cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, PartitionPlan* plan);
 cudaError_t launch_partition_insert(const PartitionLaunch& L, Table t, const PartitionPlan& plan,
-                                    cudaStream_t st);
+                                    cudaStream_t st, int blocks_per_sm = 8);
 u32 partition_count();
 
 // RASTER' cluster points (points.cu)

@@ -973,9 +973,14 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     }
     plan->units.clear();
-    for (u32 p = 0; p < kParts; ++p)
+    plan->single_units = true;
+    for (u32 p = 0; p < kParts; ++p) {
+        if (base[p + 1] - base[p] > kUnit) plan->single_units = false;
         for (u32 lo = base[p]; lo < base[p + 1]; lo += kUnit)
             plan->units.push_back(make_uint4(lo, std::min(base[p + 1], lo + kUnit), p, 0));
+    }
+    plan->units_dev = c.units;
+    plan->dcnt_dev = c.dcnt;
     const u32 U = (u32)plan->units.size();
     plan->dcnt.assign(U, 0);
     plan->pair_off.assign(U + 1, 0);
@@ -1009,13 +1014,15 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
 // Phase 2: KP3 folding the pairs (and the raw points of overflowed units)
 // into the table.
 cudaError_t launch_partition_insert(const PartitionLaunch& L, Table t, const PartitionPlan& plan,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, int blocks_per_sm) {
     const u64 n = L.n;
     const Mix m = make_mix(L.key_bits);
     const Carve c = carve(L.scratch, n);
     const u32 U = (u32)plan.units.size();
     if (U == 0) return cudaSuccess;
-    k_part_insert<<<(int)std::min<u32>(U, (u32)L.n_sm * 8), 256, 0, st>>>(c.units, U, c.dcnt,
+    // (beside K2 and K3 on another stream a small grid leaves them room: the
+    // inserts are bound by random DRAM sectors, not by threads in flight)
+    k_part_insert<<<(int)std::min<u32>(U, (u32)(L.n_sm * blocks_per_sm)), 256, 0, st>>>(c.units, U, c.dcnt,
                                                                           L.pkey, L.pcnt, t,
                                                                           L.ctr);
     for (u32 u = 0; u < U; ++u)

@@ -105,6 +105,41 @@ def test_pipeline_reuse_single_rank(tmp_path):
         dist.destroy_process_group()
 
 
+def _nccl_worker(rank, world, port, path, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda:0"))
+    try:
+        pts = np.load(path)
+        gp = D.params(3)
+        flat = cluster_distributed(torch.from_numpy(pts).cuda(), gp, device=0)
+        np.savez(os.path.join(out_dir, "nccl.npz"), tx=flat.tx, ty=flat.ty,
+                 count=flat.count.astype(np.uint64), cid=flat.cluster_id,
+                 n=np.array([flat.n_clusters, flat.stats.n_points]),
+                 backend=np.array([dist.get_backend() == "nccl"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_branch_single_rank(tmp_path):
+    """The NCCL branch of the exchanges (device tensors on the wire:
+    all_reduce of the column histogram, all_to_all_single of the [m, 2]
+    pairs, the all_gathers of the border join) on a one-rank NCCL group -
+    one GPU is all this box has; the two-rank runs above go over gloo."""
+    pts = D.generate(D.spec(3, 0.05), shuffle_seed=6)
+    path = tmp_path / "pts.npy"
+    np.save(path, pts)
+    mp.start_processes(_nccl_worker, args=(1, _free_port(), str(path), str(tmp_path)), nprocs=1,
+                       join=True, start_method="spawn")
+    ref = oracle(pts, D.params(3))
+    o = np.load(tmp_path / "nccl.npz")
+    assert bool(o["backend"][0])
+    assert np.array_equal(o["tx"], ref.tx) and np.array_equal(o["ty"], ref.ty)
+    assert np.array_equal(o["count"], ref.count.astype(np.uint64))
+    assert np.array_equal(o["cid"], ref.cluster_id)
+    assert o["n"].tolist() == [ref.n_clusters, len(pts)]
+
+
 def _worker(rank, world, port, path, cfg, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)

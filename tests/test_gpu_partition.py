@@ -55,6 +55,15 @@ pl = Pipeline(gp)
 st = pl.run(dev)
 ref = O.port_cluster(pts, gp)
 assert_same(pl.flat(), ref)
+if case == "config4_slice_shuffled":
+    # labels of an ORDERED buffer after a partitioned run: K4 resolves tiles
+    # through the table's SIG marks, whose slots were never recorded when K2
+    # ran on the pairs (k_find_slots), and the table was filled beside K2/K3
+    gen = D.generate(D.spec(4, 0.02))
+    got = pl.label_points(torch.from_numpy(gen).cuda()).cpu().numpy()
+    assert np.array_equal(got, O.port_labels(gen, gp, ref))
+    got = pl.label_points(dev).cpu().numpy()  # and of the unordered buffer itself
+    assert np.array_equal(got, O.port_labels(pts, gp, ref))
 assert st.n_points == len(pts) and st.n_skipped == int(np.count_nonzero(
     ~((pts[:, 0] >= gp.bounds.x_min) & (pts[:, 0] <= gp.bounds.x_max)
       & (pts[:, 1] >= gp.bounds.y_min) & (pts[:, 1] <= gp.bounds.y_max))))
@@ -108,6 +117,12 @@ def test_one_pass_scatter_overflow_falls_back():
 
 def test_auto_probe_picks_a_correct_path():
     _run("config4_slice_shuffled")
+
+
+def test_k2_on_the_table_after_a_partitioned_run():
+    """RG_PAIRS_K2=0: KP3 on the main stream and K2 scanning the table (the
+    default filters the pairs while KP3 runs beside it)."""
+    _run("config4_slice_shuffled", RG_PAIRS_K2="0")
 
 
 def test_multi_round_partitions():
