@@ -1,5 +1,5 @@
 import torch, sys
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, str(__import__('pathlib').Path(__file__).resolve().parents[1]))
 from paper_1907_03620_b200 import datagen as D
 s = D.spec(4); n = D.count(s)
 host = torch.empty((n, 2), dtype=torch.float64, pin_memory=True); D.generate_into(s, host.data_ptr())

@@ -1,5 +1,5 @@
 import sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, str(__import__('pathlib').Path(__file__).resolve().parents[1]))
 import torch
 from paper_1907_03620_b200 import datagen as D
 from paper_1907_03620_b200.raster import Pipeline
