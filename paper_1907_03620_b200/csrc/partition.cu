@@ -593,34 +593,48 @@ __global__ void k_part_commit(Counters* ctr, const u64* inout) {
 // table: rounds split the residuals by a hash, R rounds (a power of two).
 __device__ __forceinline__ u32 round_of(u32 r, u32 R) { return ((r * 0x85EBCA6Bu) >> 16) & (R - 1); }
 
-// Insert `c` occurrences of residual r into the shared-memory table.
+// Insert `c` occurrences of residual r into the shared-memory table: 8 Ki
+// buckets of two adjacent key slots, read with one 64-bit load. A warp's
+// lanes run the probe loop until the slowest has found its slot, so what
+// counts is the longest probe sequence among 32 lanes; two-slot buckets cut
+// the chance that a lane must move on from 30 % to 12 % per step at config
+// 4's load (37 %), i.e. about 2.6 instead of 4.7 loop trips per warp.
 __device__ __forceinline__ void agg_insert(u32* skey, u32* scnt, u32* occ, u32* over, u32 r,
                                            u32 c) {
     const u32 k = r + 1;
-    u32 s = (r * 0x9E3779B1u) >> (32 - 14);
+    constexpr u32 kBuckets = kAggSlots / 2;
+    u32 b = (r * 0x9E3779B1u) >> (32 - 13);
+    static_assert(kBuckets == 1u << 13, "bucket hash width");
     for (u32 probes = 0;; ++probes) {
-        if (probes == kAggSlots) {  // full table: the unit is redone in more rounds
+        if (probes == 2 * kAggSlots) {  // full table: the unit is redone in more rounds
             *over = 1;
             return;
         }
-        const u32 cur = skey[s];
-        if (cur == k) {
-            atomicAdd(&scnt[s], c);
-            return;
-        }
-        if (cur == 0) {
+        uint2 kk;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                     : "=r"(kk.x), "=r"(kk.y)
+                     : "r"((u32)__cvta_generic_to_shared(skey + 2 * b))
+                     : "memory");
+        u32 s;
+        if (kk.x == k) {
+            s = 2 * b;
+        } else if (kk.y == k) {
+            s = 2 * b + 1;
+        } else if (kk.x == 0 || kk.y == 0) {
+            s = 2 * b + (kk.x == 0 ? 0u : 1u);
             const u32 old = atomicCAS(&skey[s], 0u, k);
             if (old == 0) {
                 atomicAdd(&scnt[s], c);
                 if (atomicAdd(occ, 1u) >= kAggMax) *over = 1;
                 return;
             }
-            if (old == k) {
-                atomicAdd(&scnt[s], c);
-                return;
-            }
+            if (old != k) continue;  // another key took the slot: look at the bucket again
+        } else {
+            b = (b + 1) & (kBuckets - 1);
+            continue;
         }
-        s = (s + 1) & (kAggSlots - 1);
+        atomicAdd(&scnt[s], c);
+        return;
     }
 }
 
@@ -661,6 +675,8 @@ __global__ void __launch_bounds__(kAggThreads, 1) k_part_agg(const u32* res, con
                 }
                 __syncthreads();
                 constexpr int kPf = 8;  // residuals per thread in flight
+                // (loading the next step's residuals while this step's are
+                // counted measured the same: 5.69 against 5.63 ms per step)
                 for (u32 i0 = lo; i0 < hi; i0 += kAggThreads * kPf) {
                     // warp-uniform exit (no barrier inside the loop)
                     if (__any_sync(kFull, *(volatile u32*)&over != 0)) break;
