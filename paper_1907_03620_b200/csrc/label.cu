@@ -260,6 +260,17 @@ __device__ __forceinline__ void ld_entry(const ulonglong2* p, u64 pol, u64& a, u
                  : "l"(p), "l"(pol));
 }
 
+// Both entries of a 32-byte bucket with ONE 256-bit load (sm_100): a warp's
+// 32 lookups go to 32 different sectors, and the load/store unit handles one
+// sector per cycle, so two 16-byte loads per bucket cost twice the cycles
+// (k_label_cells was bound by the LSU data pipe, 71 % of its peak).
+__device__ __forceinline__ void ld_bucket(const ulonglong2* p, u64 pol, u64& a0, u64& m0, u64& a1,
+                                          u64& m1) {
+    asm volatile("ld.global.L2::cache_hint.v4.u64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(a0), "=l"(m0), "=l"(a1), "=l"(m1)
+                 : "l"(p), "l"(pol));
+}
+
 // Cell entry or nullptr (build-time lookups use pol = 0: no hint needed).
 __device__ __forceinline__ const ulonglong2* cell_find(const ulonglong2* tab, u64 nb, u32 cell,
                                                        u64) {
@@ -340,8 +351,12 @@ __global__ void __launch_bounds__(256) k_label_cells(const double2* xy, u64 n, G
                 u64 b = cell_bucket(cell, nb);
                 while (true) {
                     u64 a0, m0, a1, m1;
+#ifdef RG_K4P_LD128
                     ld_entry(tab + 2 * b, pol_tab, a0, m0);
                     ld_entry(tab + 2 * b + 1, pol_tab, a1, m1);
+#else
+                    ld_bucket(tab + 2 * b, pol_tab, a0, m0, a1, m1);
+#endif
                     if (cell_try(a0, m0, a1, m1, cell, bit, ids, c)) break;
                     b = b + 1 == nb ? 0 : b + 1;
                 }

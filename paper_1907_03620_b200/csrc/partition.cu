@@ -9,26 +9,29 @@
 // the points are instead partitioned by tile so that every tile's points
 // meet in one block's shared memory:
 //
-//   KP0 k_part_hist    stream the points once; per 64 Ki-point tile, a
-//                      shared-memory histogram of the 2048 partitions;
-//   (scan)             partition-major exclusive scan of the histograms:
-//                      every (partition, tile) run gets its exact place;
-//   KP1 k_part_scatter stream the points again; in 16 Ki-point rounds,
-//                      order them by partition in shared memory and write
-//                      each point's 32-bit residual key in runs (no global
-//                      atomics);
-//   KP2 k_part_agg     one block per work unit (up to 256 Ki points of one
+//   scatter            every in-bounds point's 32-bit residual key lands in
+//                      its partition's region. Default: the one-pass scatter
+//                      (KQ0 k_part_sample, KQp k_part_plan, KQ1 k_part_stream:
+//                      regions sized from a sample, per-block write-combining
+//                      rings, whole-sector writes; see the KQ section below).
+//                      Fallback, for a hot partition or a region that would
+//                      overflow: KP0 k_part_hist (exact per-tile histograms
+//                      of the 2048 partitions), a partition-major scan, and
+//                      KP1 k_part_scatter (the points again, 16 Ki-point
+//                      rounds ordered by partition in shared memory);
+//   KP2 k_part_agg     one block per work unit (up to 512 Ki entries of one
 //                      partition) counts its residuals in a shared-memory
-//                      hash table (16 Ki slots; more rounds when a unit has
-//                      more tiles) and writes its (key, count) pairs into
-//                      its own slab;
-//   KP3 k_part_insert  folds the pairs into the HBM table (one CAS + RED per
-//                      distinct tile of a unit), after the host has grown
-//                      the table to fit them.
+//                      hash table (16 Ki slots in two-slot buckets; more
+//                      rounds when a unit has more tiles) and writes its
+//                      (key, count) pairs into its own slab;
+//   KP3 k_part_insert  folds the pairs into the HBM table (one 128-bit CAS
+//                      per distinct tile of a unit), after the host has
+//                      grown the table to fit them. In rg_cluster it runs on
+//                      a side stream while K2 filters the pairs (api.cu).
 //
-// Config 4 in a random order: 9.2 ms per step against 21.7 ms with K1 (whose
-// cache then misses on every point). Ordered inputs keep K1 (an order probe
-// in api.cu decides).
+// Config 4 in a random order: 5.6 ms per step against 21.7 ms with K1 (whose
+// cache then misses on every point) and 8.5 ms with the exact scatter.
+// Ordered inputs keep K1 (an order probe in api.cu decides).
 //
 // A partition is the low 11 bits of a bijective mix of the packed key
 // (multiply by an odd constant mod 2^B, then xor-shift by ceil(B/2)); the
