@@ -390,6 +390,7 @@ struct rg_ctx {
     const double* probe_ptr = nullptr;  // last probed buffer and its verdict
     u64 probe_n = 0;
     bool probe_unordered = false;
+    float probe_new_ratio = 0.f;  // share of the probed points that opened a new tile
     void* sort_temp = nullptr;
     size_t sort_temp_bytes = 0;
     u64 n_roots = 0, n_kept = 0;
@@ -754,6 +755,7 @@ bool buffer_unordered(rg_ctx* ctx, const double* xy, u64 n) {
     ctx->probe_n = n;
     ctx->probe_fp = ctx->order_probe[2];
     ctx->probe_unordered = valid > 0 && distinct * 5 > valid * 3;  // > 60 % open a new tile
+    ctx->probe_new_ratio = valid ? (float)((double)distinct / (double)valid) : 0.f;
     if (g_debug)
         std::fprintf(stderr, "[rg] order probe n=%llu: %llu of %llu sampled points open a tile -> %s\n",
                      (unsigned long long)n, (unsigned long long)distinct,
@@ -877,6 +879,17 @@ rg_status k1_launch_round(rg_ctx* ctx) {
     L.partial_out = ctx->part[1 - r.pin];
     L.budget = (soft - ctx->used) / r.W;
     L.narrow = ctx->narrow;
+    // An input whose evictions mostly claim NEW keys (config 5: 60M noise and
+    // chain tiles, ~30 % of the probed points open a tile) installs key and
+    // count with one 128-bit CAS: K1 3.52 -> 3.17 ms; for config 4 (2 %) the
+    // 64-bit claim + RED is faster (1.55 against 1.59 ms).
+    static const int c128_mode = [] {  // RG_K1_CLAIM128=0 / =1 forces it (A/B)
+        const char* v = std::getenv("RG_K1_CLAIM128");
+        return v ? (std::strcmp(v, "0") == 0 ? 0 : 1) : -1;
+    }();
+    L.claim128 = c128_mode >= 0 ? c128_mode != 0
+                                : (ctx->probe_ptr == r.xy && ctx->probe_n == r.n &&
+                                   ctx->probe_new_ratio >= 0.2f);
     CK(launch_contract(L, ctx->st));
     ++ctx->launches;
     CK(cudaEventRecord(ctx->ev_c1, ctx->st));

@@ -100,6 +100,7 @@ struct K1State {
 // lanes in parallel (the divergent, latency-bound part of a miss is paid
 // once per 32 misses instead of once per row). Placeholder entries (a miss
 // that filled an empty cache slot reserved one) carry kEmpty and are skipped.
+template <bool kC128 = false>
 __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State& s, int lane) {
     u32 c = 0, ph = 0;
     for (u32 e = lane; e < s.slen; e += 32) {
@@ -108,7 +109,8 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
 #ifdef RG_K1_NOFLUSH  // experiment: drop evictions (results are wrong)
             c += (w.scnt[e] == 12345) ? 1u : 0u;
 #else
-            c += table_add_cas(t, k, w.scnt[e]) ? 1u : 0u;
+            // (claim-heavy inputs install key and count with one 128-bit CAS)
+            c += (kC128 ? table_add_cas128(t, k, w.scnt[e]) : table_add_cas(t, k, w.scnt[e])) ? 1u : 0u;
 #endif
             s.added += w.scnt[e];
         } else {
@@ -135,7 +137,7 @@ __device__ __forceinline__ void flush_stage(const Table& t, WarpSmem& w, K1State
 // with count 0; then every missing lane whose key now owns its slot adds
 // 1, and the others (a different key won the slot in this row) stage
 // (key, 1) themselves.
-template <bool kNarrow, bool kPf>
+template <bool kNarrow, bool kPf, bool kC128>
 __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
                                               int lane, u32 lt_mask, u32 budget) {
@@ -187,7 +189,7 @@ __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, con
             s.slen += ns;
             s.pot += ns;
             __syncwarp();
-            if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
+            if (s.slen > kStageCap - 32 * kBatch) flush_stage<kC128>(t, w, s, lane);
         }
     }
     return s.pot >= budget;
@@ -205,7 +207,7 @@ __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, con
 // placeholder if the slot was empty) and installs its key with count 0;
 // every missing point whose key now owns its slot adds 1, the others stage
 // (key, 1). Each winner and each loser adds one staged entry.
-template <bool kNarrow, bool kPf>
+template <bool kNarrow, bool kPf, bool kC128>
 __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, const double* x,
                                               const double* y, WarpSmem& w, K1State& s,
                                               int lane, u32 lt_mask, u32 budget) {
@@ -282,7 +284,7 @@ __device__ __forceinline__ bool process_batch(const Grid& g, const Table& t, con
     s.pot += pos - s.slen;
     s.slen = pos;
     __syncwarp();
-    if (s.slen > kStageCap - 32 * kBatch) flush_stage(t, w, s, lane);
+    if (s.slen > kStageCap - 32 * kBatch) flush_stage<kC128>(t, w, s, lane);
     return s.pot >= budget;
 }
 #endif  // RG_K1_ROWWISE
@@ -344,7 +346,7 @@ constexpr int kK1Unroll = RG_K1_UNROLL;  // batches per trip of run_segment's lo
 // into its own ring column, so no cross-lane synchronisation is needed
 // around the ring. Returns the row index at which the warp ran out of
 // budget, or nr.
-template <bool kAligned, bool kNarrow, bool kFullRows, bool kPf>
+template <bool kAligned, bool kNarrow, bool kFullRows, bool kPf, bool kC128>
 __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy_base, u32 nr,
                                            u32 valid, double2 (*ring)[32], const Grid& g,
                                            const Table& t, WarpSmem& w, K1State& st, int lane,
@@ -388,7 +390,7 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
         for (int b = 0; b < kBatch; ++b) st.added += (x[b] + y[b] > 1e300) ? 1 : 0;
         const bool over = false;
 #else
-        const bool over = process_batch<kNarrow, kPf>(g, t, x, y, w, st, lane, lt_mask, budget);
+        const bool over = process_batch<kNarrow, kPf, kC128>(g, t, x, y, w, st, lane, lt_mask, budget);
 #endif
         if (over) return j + kBatch < nr ? j + kBatch : nr;
     }
@@ -400,7 +402,7 @@ __device__ __forceinline__ u32 run_segment(const double2* base, const double* xy
 // once every lane has read it. `phase` carries the stages' mbarrier parities
 // across segments. Same return convention as run_segment.
 constexpr int kStages = kRing / kBatch;
-template <bool kNarrow, bool kPf>
+template <bool kNarrow, bool kPf, bool kC128>
 __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 valid,
                                                double2 (*ring)[32], u64* bar, u32& phase,
                                                const Grid& g, const Table& t, WarpSmem& w,
@@ -434,7 +436,7 @@ __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 v
 #endif
             issue(b + kStages);
         }
-        if (process_batch<kNarrow, kPf>(g, t, x, y, w, st, lane, lt_mask, budget)) {
+        if (process_batch<kNarrow, kPf, kC128>(g, t, x, y, w, st, lane, lt_mask, budget)) {
             done_b = b + 1;
             break;
         }
@@ -448,8 +450,10 @@ __device__ __forceinline__ u32 run_segment_tma(const double2* src, u32 nr, u32 v
     return done_b < nb ? done_b * kBatch : nr;
 }
 
-template <bool kAligned, bool kNarrow, bool kTma, bool kPf = false>
-__global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params P) {
+template <bool kAligned, bool kNarrow, bool kTma, bool kPf = false, bool kC128 = false>
+// (the 128-bit claim variant is held to the others' 9 blocks per SM: the
+// launch is sized for the slowest variant's residency)
+__global__ void __launch_bounds__(kThreads, kC128 ? 9 : RG_K1_MINBLOCKS) k_contract(K1Params P) {
     __shared__ WarpSmem s_warp[kWarpsPerBlock];
     __shared__ __align__(16) double2 s_ring[kWarpsPerBlock][kRing][32];
     __shared__ u64 s_bar[kWarpsPerBlock][kStages];
@@ -545,13 +549,13 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
         const double* xy_base = P.xy + 2 * p0;
         u32 done;
         if (kTma)
-            done = run_segment_tma<kNarrow, kPf>(pts + p0, nr, valid, ring, bar, phase, g, t, w, st,
+            done = run_segment_tma<kNarrow, kPf, kC128>(pts + p0, nr, valid, ring, bar, phase, g, t, w, st,
                                             lane, lt_mask, pol, P.budget);
         else if (valid == nr * 32 && nr % kBatch == 0)
-            done = run_segment<kAligned, kNarrow, true, kPf>(base, xy_base, nr, valid, ring, g, t, w,
+            done = run_segment<kAligned, kNarrow, true, kPf, kC128>(base, xy_base, nr, valid, ring, g, t, w,
                                                         st, lane, lt_mask, pol, P.budget);
         else
-            done = run_segment<kAligned, kNarrow, false, kPf>(base, xy_base, nr, valid, ring, g, t, w,
+            done = run_segment<kAligned, kNarrow, false, kPf, kC128>(base, xy_base, nr, valid, ring, g, t, w,
                                                          st, lane, lt_mask, pol, P.budget);
         if (!kTma) cp_async_wait<0>();
         n_valid += min((u64)done * 32, (u64)valid);
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, RG_K1_MINBLOCKS) k_contract(K1Params
     }
 
     // Write back staged entries and the cache.
-    flush_stage(t, w, st, lane);
+    flush_stage<kC128>(t, w, st, lane);
     for (int i = lane; i < kCacheSlots; i += 32) {
         const u64 k = KeyOps<kNarrow>::table_key(w.ckey[i], g.bits_y);
         if (k != kEmpty) {
@@ -1070,15 +1074,16 @@ static int g_k1_warps_per_sm = 0;
 // overshoot its load target (see ingest_device in api.cu).
 int contract_max_warps(int n_sm) {
     if (!g_k1_warps_per_sm) {
-        int b[6] = {0, 0, 0, 0, 0, 0};
+        int b[7] = {0, 0, 0, 0, 0, 0, 0};
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[0], k_contract<true, true, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[1], k_contract<true, false, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[2], k_contract<false, true, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[3], k_contract<false, false, false>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[4], k_contract<true, true, true>, kThreads, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[5], k_contract<true, true, false, true>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b[6], k_contract<true, true, false, false, true>, kThreads, 0);
         int m = b[0];
-        for (int i = 1; i < 6; ++i) m = b[i] < m ? b[i] : m;
+        for (int i = 1; i < 7; ++i) m = b[i] < m ? b[i] : m;
         g_k1_warps_per_sm = (m < 1 ? 1 : m) * kWarpsPerBlock;
     }
     return g_k1_warps_per_sm * n_sm;
@@ -1117,6 +1122,8 @@ cudaError_t launch_contract(const ContractLaunch& L, cudaStream_t st) {
     }();
     if (aligned && L.narrow && tma)
         k_contract<true, true, true><<<blocks, kThreads, 0, st>>>(P);
+    else if (aligned && L.narrow && L.claim128)
+        k_contract<true, true, false, false, true><<<blocks, kThreads, 0, st>>>(P);
     else if (aligned && L.narrow && prefetch)
         k_contract<true, true, false, true><<<blocks, kThreads, 0, st>>>(P);
     else if (aligned && L.narrow)

@@ -22,6 +22,7 @@ struct ContractLaunch {
     Partial* partial_out;
     u64 budget;
     bool narrow;  // canvas column/row indices fit int32
+    bool claim128 = false;  // most evictions claim new keys: one 128-bit CAS per claim
 };
 
 int contract_max_warps(int n_sm);
