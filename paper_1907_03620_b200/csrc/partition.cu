@@ -303,7 +303,7 @@ constexpr u32 kQC = 24;                 // entries per write-combining buffer
 constexpr int kQThr = 1024;
 constexpr int kQPer = 8;                // points per thread per round
 constexpr u32 kQRound = kQThr * kQPer;  // 8192
-constexpr u32 kQHot = 6;                // expected points per partition and round above which the exact path is taken
+constexpr u32 kQHot = 8;                // expected points per partition and round (mean 4) above which the exact path is taken: a ring has room for 17
 constexpr size_t kStreamSmem = (size_t)(kParts * kQC + 4 * kParts) * 4;
 constexpr u32 kSkip = 0xffffffffu;
 
@@ -744,8 +744,11 @@ __global__ void k_part_insert_raw(const u32* res, u32 b0, u32 b1, u32 p, Mix m, 
                                   Counters* ctr) {
     u32 claims = 0;
     for (u64 i = b0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < b1;
-         i += (u64)gridDim.x * blockDim.x)
-        claims += table_add(t, unmix(m, ((u64)res[i] << kPBits) | p), 1) ? 1u : 0u;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 r = res[i];
+        if (r == 0xffffffffu) continue;  // head-room of the one-pass scatter's sub-regions
+        claims += table_add(t, unmix(m, ((u64)r << kPBits) | p), 1) ? 1u : 0u;
+    }
     claims = __reduce_add_sync(__activemask(), claims);
     if ((threadIdx.x & 31) == 0 && claims) atomicAdd(&ctr->used, (u64)claims);
 }

@@ -130,9 +130,11 @@ def test_multi_round_partitions():
     _run("uniform_many_tiles", RG_INGEST="part")
 
 
-def test_per_point_fallback():
-    """One round allowed: partitions that overflow it take the per-point path."""
-    _run("uniform_many_tiles", RG_INGEST="part", RG_PART_MAX_ROUNDS="1")
+@pytest.mark.parametrize("scatter", ["exact", "stream"])
+def test_per_point_fallback(scatter):
+    """One round allowed: partitions that overflow it take the per-point path
+    (after the one-pass scatter it must skip the sub-regions' head-room)."""
+    _run("uniform_many_tiles", RG_INGEST="part", RG_PART_MAX_ROUNDS="1", RG_PART=scatter)
 
 
 def test_order_verdict_follows_buffer_content():
