@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(1024) k_part_sample(const double2* xy, u64 n, 
 //   capb[p]   entries of one block's sub-region of partition p (multiple of 8)
 //   pstart[p] first entry of partition p's region; pstart[kParts] = total
 __global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, u32 nblk,
-                                                    u64 res_cap, float sigmas, u32* capb,
-                                                    u32* pstart, u32* plan) {
+                                                    u64 res_cap, float sigmas, u32 hot_limit,
+                                                    u32* capb, u32* pstart, u32* plan) {
     __shared__ u64 wsum[32];
     __shared__ u32 smax;
     static_assert(kParts == 2048, "two partitions per thread");
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, 
             const bool big = wi > res_cap;
             pstart[kParts] = big ? 0u : (u32)wi;
             const u64 S = shist[kParts];
-            const bool hot = (u64)smax * kQRound > (u64)kQHot * S;
+            const bool hot = (u64)smax * kQRound > (u64)hot_limit * S;
             plan[kPlFallback] = big ? 2u : (hot ? 1u : 0u);
             plan[kPlOverflow] = 0;
         }
@@ -926,6 +926,13 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         const char* v = std::getenv("RG_PART_SIGMA");
         return v ? (float)std::atof(v) : 6.0f;
     }();
+    // RG_PART_HOT: test knob; a large value sends a skewed input down the
+    // one-pass scatter, where the hot partition's ring overflows all the time
+    static const u32 hot_limit = [] {
+        const char* v = std::getenv("RG_PART_HOT");
+        const long h = v ? std::atol(v) : 0;
+        return h > 0 ? (u32)h : kQHot;
+    }();
     std::vector<u32> base(kParts + 1);
     bool streamed = false;
     plan->launches = 0;
@@ -940,8 +947,8 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         const u64 n_win = ((n + 7) / 8 + stride - 1) / stride;
         k_part_sample<<<(int)std::min<u64>((n_win * 8 + 1023) / 1024, (u64)L.n_sm * 2), 1024, 0, st>>>(
             xy, n, L.g, m, stride, c.shist);
-        k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, nblk, res_cap, sigmas, c.capb, c.pstart,
-                                        c.plan);
+        k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, nblk, res_cap, sigmas, hot_limit, c.capb,
+                                        c.pstart, c.plan);
         StreamArgs A{xy, n, L.g, m, c.capb, c.pstart, c.plan, c.res, c.inout};
         if (L.narrow)
             k_part_stream<true><<<(int)nblk, kQThr, kStreamSmem, st>>>(A);

@@ -109,6 +109,13 @@ def test_both_scatters(case, scatter):
     _run(case, RG_INGEST="part", RG_PART=scatter)
 
 
+def test_one_pass_scatter_with_a_full_ring():
+    """Config 5's hot tile forced down the one-pass scatter: its partition's
+    ring is full in every round, so most of its points take the direct path
+    to the sub-region (unaligned sector writes from then on)."""
+    _run("config5_slice_shuffled", RG_INGEST="part", RG_PART="stream", RG_PART_HOT="1000000")
+
+
 def test_one_pass_scatter_overflow_falls_back():
     """Sub-regions sized below the estimate overflow; the call is redone on
     the exact path and the counters are not double counted."""
