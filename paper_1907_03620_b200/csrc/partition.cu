@@ -340,9 +340,12 @@ __global__ void __launch_bounds__(1024) k_part_sample(const double2* xy, u64 n, 
 // One block: capacities, region starts, fallback decision.
 //   capb[p]   entries of one block's sub-region of partition p (multiple of 8)
 //   pstart[p] first entry of partition p's region; pstart[kParts] = total
-__global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, u32 nblk,
-                                                    u64 res_cap, float sigmas, u32 hot_limit,
-                                                    u32* capb, u32* pstart, u32* plan) {
+// `share` = the largest part of the rounds one block takes (rounds go round
+// robin, so a block has floor or ceil(n_rounds / nblk) of them).
+__global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, float share,
+                                                    u32 nblk, u64 res_cap, float sigmas,
+                                                    u32 hot_limit, u32* capb, u32* pstart,
+                                                    u32* plan) {
     __shared__ u64 wsum[32];
     __shared__ u32 smax;
     static_assert(kParts == 2048, "two partitions per thread");
@@ -356,8 +359,8 @@ __global__ void __launch_bounds__(1024) k_part_plan(const u32* shist, u64 frac, 
         const u32 p = 2 * threadIdx.x + q;
         const u32 sp = shist[p];
         mx = max(mx, sp);
-        const float est = (float)sp * (float)frac / (float)nblk;
-        const float sd = sqrtf(est * (1.0f + (float)frac / (float)nblk));
+        const float est = (float)sp * (float)frac * share;
+        const float sd = sqrtf(est * (1.0f + (float)frac * share));
         const u32 c = ((u32)fmaxf(est + sigmas * sd, 0.0f) + 16 + 7) & ~7u;
         capb[p] = c;
         tot[q] = (u64)c * nblk;
@@ -947,8 +950,9 @@ cudaError_t launch_partition_count(const PartitionLaunch& L, cudaStream_t st, Pa
         const u64 n_win = ((n + 7) / 8 + stride - 1) / stride;
         k_part_sample<<<(int)std::min<u64>((n_win * 8 + 1023) / 1024, (u64)L.n_sm * 2), 1024, 0, st>>>(
             xy, n, L.g, m, stride, c.shist);
-        k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, nblk, res_cap, sigmas, hot_limit, c.capb,
-                                        c.pstart, c.plan);
+        const float share = (float)((n_rounds + nblk - 1) / nblk) / (float)n_rounds;
+        k_part_plan<<<1, 1024, 0, st>>>(c.shist, stride, share, nblk, res_cap, sigmas, hot_limit,
+                                        c.capb, c.pstart, c.plan);
         StreamArgs A{xy, n, L.g, m, c.capb, c.pstart, c.plan, c.res, c.inout};
         if (L.narrow)
             k_part_stream<true><<<(int)nblk, kQThr, kStreamSmem, st>>>(A);
