@@ -37,7 +37,7 @@ elif case == "uniform_many_tiles":
     pts = np.concatenate([rng.uniform([-180, -90], [180, 90], size=(30_000_000, 2)),
                           rng.normal([10, 10], 0.01, size=(2_000_000, 2))])
     rng.shuffle(pts)
-elif case == "config5_slice_shuffled":  # a hot tile: the one-pass scatter's plan takes the exact path
+elif case == "config5_slice_shuffled":  # a hot tile: its partition's ring is full in every round
     gp = D.params(5)
     pts = D.generate(D.spec(5, 0.05), shuffle_seed=6)  # 10M points
 elif case == "unaligned":
@@ -105,15 +105,15 @@ def test_forced_partition_path(case):
                                   "config5_slice_shuffled"])
 def test_both_scatters(case, scatter):
     """KP0 + KP1 (exact histogram) and KQ0 + KQ1 (sampled plan, one pass) give
-    the oracle's counts; config 5's hot tile makes the plan fall back."""
+    the oracle's counts; config 5's hot tile keeps one ring full (its points
+    go straight to the sub-region)."""
     _run(case, RG_INGEST="part", RG_PART=scatter)
 
 
-def test_one_pass_scatter_with_a_full_ring():
-    """Config 5's hot tile forced down the one-pass scatter: its partition's
-    ring is full in every round, so most of its points take the direct path
-    to the sub-region (unaligned sector writes from then on)."""
-    _run("config5_slice_shuffled", RG_INGEST="part", RG_PART="stream", RG_PART_HOT="1000000")
+def test_one_pass_scatter_hot_limit_falls_back():
+    """RG_PART_HOT=6: the plan sends config 5's hot partition to the exact
+    scatter (the default limit only stops half a round in one partition)."""
+    _run("config5_slice_shuffled", RG_INGEST="part", RG_PART="stream", RG_PART_HOT="6")
 
 
 def test_one_pass_scatter_overflow_falls_back():
