@@ -59,7 +59,6 @@ constexpr u32 kParts = 1u << kPBits;
 constexpr u64 kPTile = 65536;          // points per histogram tile
 constexpr int kPThreads = 512;
 constexpr int kPSub = 8;               // points per thread per sub-chunk
-constexpr u32 kPSubN = kPThreads * kPSub;
 constexpr u32 kAggSlots = 1u << 14;    // shared-memory hash table (KP2)
 constexpr u32 kAggMax = 12288;         // distinct tiles per round (75 % load)
 constexpr u32 kMaxRounds = 64;
