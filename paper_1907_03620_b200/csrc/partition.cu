@@ -762,21 +762,32 @@ __global__ void k_part_insert_raw(const u32* res, u32 b0, u32 b1, u32 p, Mix m, 
     if ((threadIdx.x & 31) == 0 && claims) atomicAdd(&ctr->used, (u64)claims);
 }
 
-// Order probe: distinct tiles among 2048 consecutive points, per sample.
+// Order probe: distinct tiles among 2048 consecutive points, per sample, and
+// how many points lie within 8 tiles of their successor (spatial order: a
+// generated or sorted input scores high, a shuffled one only as often as two
+// random points share a hot spot). out[0] += distinct, out[1] += valid |
+// near << 32.
 __global__ void __launch_bounds__(256) k_order_probe(const double2* xy, u64 n, Grid g, u64 stride,
                                                      u64* out) {
     __shared__ u64 keys[4096];
-    __shared__ u32 distinct, valid;
+    __shared__ u32 distinct, valid, near;
     for (u32 i = threadIdx.x; i < 4096; i += 256) keys[i] = kEmpty;
-    if (threadIdx.x == 0) distinct = valid = 0;
+    if (threadIdx.x == 0) distinct = valid = near = 0;
     __syncthreads();
     const u64 b = blockIdx.x * stride;
+    const u64 ymask = (1ull << g.bits_y) - 1;
     for (u32 j = threadIdx.x; j < 2048; j += 256) {
         const u64 i = b + j;
         if (i >= n) break;
         u64 k;
         if (!point_key(g, xy[i], k)) continue;
         atomicAdd(&valid, 1u);
+        u64 k2;
+        if (i + 1 < n && point_key(g, xy[i + 1], k2)) {
+            const long long dx = (long long)(k >> g.bits_y) - (long long)(k2 >> g.bits_y);
+            const long long dy = (long long)(k & ymask) - (long long)(k2 & ymask);
+            if (dx >= -8 && dx <= 8 && dy >= -8 && dy <= 8) atomicAdd(&near, 1u);
+        }
         u32 s = (u32)((k * 0x9E3779B97F4A7C15ull) >> 52);
         while (true) {
             const u64 old = atomicCAS(&keys[s], kEmpty, k);
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(256) k_order_probe(const double2* xy, u64 n, G
     __syncthreads();
     if (threadIdx.x == 0) {
         atomicAdd(out, (u64)distinct);
-        atomicAdd(out + 1, (u64)valid);
+        atomicAdd(out + 1, (u64)valid | ((u64)near << 32));
     }
 }
 
