@@ -730,13 +730,20 @@ constexpr int kP2Items = 12;
 constexpr u64 kBktMaxCol = RG_BKT_MAX_COL;  // 4096 + kBktMaxCol <= 512 * kP2Items
 constexpr size_t p2_smem(int threads) { return (size_t)threads * kP2Items * (8 + 4 + 4 + 2); }
 
-__global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 n, u32 bits_y,
-                                                            const u32* col_off, u32* cur,
-                                                            u32 nbkt, u32 shift, u64* k_out,
-                                                            u32* v_out) {
+// (n and the bucket count are read on the device: the launch may be sized
+// for an upper bound of n; `nbkt_cap` >= the bucket count lays out the
+// shared memory; rs = bucket starts, then the scatter cursors, as
+// k_col_scan left them)
+__global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, const u64* n_p,
+                                                            u32 bits_y, const u32* col_off,
+                                                            u32* rs, u32 nbkt_cap, u32 shift,
+                                                            u64* k_out, u32* v_out) {
     extern __shared__ u32 sh_p1[];
+    const u64 n = *n_p;
+    const u32 nbkt = (u32)((n + (1ull << shift) - 1) >> shift);
+    u32* cur = rs + nbkt + 1;
     u32* hist = sh_p1;
-    u32* base = sh_p1 + nbkt;
+    u32* base = sh_p1 + nbkt_cap;
     for (u64 t0 = blockIdx.x * (u64)kP1Tile; t0 < n; t0 += (u64)gridDim.x * kP1Tile) {
         for (u32 b = threadIdx.x; b < nbkt; b += kP1Threads) hist[b] = 0;
         __syncthreads();
@@ -790,10 +797,12 @@ __global__ void __launch_bounds__(kP1Threads) k_bkt_scatter(const u64* key, u64 
 // column length, then union-find parent) and the slot's column start (u16).
 template <bool kUnion, int kP2Threads, int kMinBlocks>
 __global__ void __launch_bounds__(kP2Threads, kMinBlocks) k_bkt_sort(const u64* kin, const u32* vin,
-                                                                     const u32* rs, u32 nbkt,
+                                                                     const u32* rs, const u64* n_p,
+                                                                     u32 shift,
                                                                      const u32* col_off, u32 bits_y,
                                                                      u64* skey, u32* perm,
                                                                      u32* parent, u32* size) {
+    const u32 nbkt = (u32)((*n_p + (1ull << shift) - 1) >> shift);
     constexpr u32 kP2Cap = kP2Threads * kP2Items;
     extern __shared__ u64 sh_p2[];
     u64* sk = sh_p2;
@@ -804,6 +813,10 @@ __global__ void __launch_bounds__(kP2Threads, kMinBlocks) k_bkt_sort(const u64* 
     for (u32 b = blockIdx.x; b < nbkt; b += gridDim.x) {
         const u32 r0 = rs[b], r1 = rs[b + 1];
         const u32 m = r1 - r0;
+        // (a bucket holds whole columns, < 4096 + the longest column: a launch
+        // that did not wait for the longest column's length must not trust it;
+        // the host sees max_col with the final counters and redoes K3 then)
+        if (m > kP2Cap) continue;
         for (u32 j = tid; j < m; j += kP2Threads) aux[j] = 0;
         // all of this thread's keys, perms and column starts in flight together
         u64 kk[kP2Items];
@@ -971,8 +984,10 @@ __global__ void __launch_bounds__(kP2Threads, kMinBlocks) k_bkt_sort(const u64* 
 
 // Edges between the last column of bucket b and the first column of bucket
 // b+1 (Chebyshev delta 1, all three offsets; no elision needed).
-__global__ void k_bkt_cross(const u64* skey, const u32* rs, u32 nbkt, const u32* col_off,
-                            u64 cols, u32 bits_y, u32* parent, u32* linked, u64* n_linked) {
+__global__ void k_bkt_cross(const u64* skey, const u32* rs, const u64* n_p, u32 shift,
+                            const u32* col_off, u64 cols, u32 bits_y, u32* parent, u32* linked,
+                            u64* n_linked) {
+    const u32 nbkt = (u32)((*n_p + (1ull << shift) - 1) >> shift);
     const int lane = threadIdx.x & 31;
     const u64 ymask = (1ull << bits_y) - 1;
     const u64 warp = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
@@ -1107,6 +1122,8 @@ static LbScratch lb_scratch(void* temp, u64 tiles, cudaStream_t st) {
 #endif
 constexpr u64 kSegSortMaxColumn = RG_SEG_MAX_COLUMN;
 
+u64 sorted_bucket_max_column() { return kBktMaxCol; }
+
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     if (L.n_sig == 0) return cudaSuccess;
     cudaError_t e;
@@ -1127,9 +1144,22 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                                                   (u32*)&L.ctr->max_col, L.flag, lb.status,
                                                   lb.ticket);
     }
-    // The exact significant count (L.n_sig may be an upper bound) and the
-    // longest column decide the sort and size every launch below.
-    if (L.check_k1_stop) {  // K1's counters ride along (its stop check was deferred)
+    const bool c1 = L.delta == 1 && !L.manhattan;
+    static const int variant = [] {
+        const char* v = std::getenv("RG_K3_SORT");
+        return v && v[0] == 's' ? 1 : (v && v[0] == 'r' ? 2 : 0);
+    }();
+    // Without the host read (L.speculate): every launch is sized for the
+    // bound L.n_sig, the kernels read the exact count on the device, and the
+    // bucketed path is taken on the assumption that no column is longer than
+    // kBktMaxCol; the caller checks max_col (and K1's stop flag) in the
+    // counters it reads at the end of the call and redoes K3 otherwise.
+    const bool spec = L.speculate && c1 && cols && L.col_cnt && variant == 0 &&
+                      (size_t)(((L.n_sig + (1ull << shift) - 1) >> shift) + 1) * 8 <= 96 * 1024;
+    if (L.speculated) *L.speculated = spec;
+    if (spec) {
+        // nothing to wait for
+    } else if (L.check_k1_stop) {  // K1's counters ride along (its stop check was deferred)
         if ((e = cudaMemcpyAsync(L.host_ctr, L.ctr, sizeof(Counters), cudaMemcpyDeviceToHost,
                                  st)) != cudaSuccess)
             return e;
@@ -1138,13 +1168,13 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                                     cudaMemcpyDeviceToHost, st)) != cudaSuccess) {
         return e;
     }
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-    if (L.check_k1_stop && L.host_ctr->stopped) {
+    if (!spec && (e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if (!spec && L.check_k1_stop && L.host_ctr->stopped) {
         if (L.launches) *L.launches = cols && L.col_cnt ? (L.col_hist_ready ? 1 : 2) : 0;
         return cudaErrorNotReady;
     }
-    const u64 n = L.host_ctr->n_sig;
-    if (std::getenv("RG_DEBUG"))
+    const u64 n = spec ? L.n_sig : L.host_ctr->n_sig;  // (an upper bound when speculating)
+    if (!spec && std::getenv("RG_DEBUG"))
         std::fprintf(stderr, "[rg] K3 sorted: n=%llu max_col=%llu\n", (unsigned long long)n,
                      (unsigned long long)L.host_ctr->max_col);
     if (n == 0) {
@@ -1153,20 +1183,14 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
     }
     const int gs = grid_for_s(n, L.n_sm, 16);
     int launches = cols && L.col_cnt ? (L.col_hist_ready ? 1 : 2) : 0;  // col_hist, col_scan
-    const u64 mcol = L.host_ctr->max_col;
+    const u64 mcol = spec ? 0 : L.host_ctr->max_col;
     const u32 nbkt = (u32)((n + (1ull << shift) - 1) >> shift);
-    const bool c1 = L.delta == 1 && !L.manhattan;
     bool bucket_counts = false;  // per-root counts already final (bucketed Chebyshev-1 path)
-    static const int variant = [] {
-        const char* v = std::getenv("RG_K3_SORT");
-        return v && v[0] == 's' ? 1 : (v && v[0] == 'r' ? 2 : 0);
-    }();
     if (cols && L.col_cnt && variant == 0 && mcol <= kBktMaxCol &&
         (size_t)nbkt * 8 <= 96 * 1024) {  // L.flag holds >= 1024 and >= n entries
         // bucketed column sort (+ fused bucket-local unions for Chebyshev 1);
         // k_col_scan left the bucket starts and the scatter cursors in flag
         u32* rs = L.flag;  // nbkt + 1 region starts, then nbkt scatter cursors
-        u32* cur = L.flag + nbkt + 1;
         const size_t sm1 = (size_t)nbkt * 2 * sizeof(u32);
         static bool attr = false;
         if (!attr) {
@@ -1180,13 +1204,13 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
         }
         const u64 t1 = (n + kP1Tile - 1) / kP1Tile;
         const int g1 = (int)std::min<u64>(t1, (u64)L.n_sm * (2048 / kP1Threads));
-        k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, n, L.bits_y, L.col_off, cur, nbkt,
-                                                   shift, L.ktmp, L.iota);
+        k_bkt_scatter<<<g1, kP1Threads, sm1, st>>>(L.sig_key, L.n_sig_dev, L.bits_y, L.col_off, rs,
+                                                   nbkt, shift, L.ktmp, L.iota);
         const int g2 = (int)std::min<u64>(nbkt, (u64)L.n_sm * 2);
         auto p2 = [&](auto kernel, int threads) {
-            kernel<<<g2, threads, p2_smem(threads), st>>>(L.ktmp, L.iota, rs, nbkt, L.col_off,
-                                                          L.bits_y, L.skey, L.perm, L.parent,
-                                                          L.size);
+            kernel<<<g2, threads, p2_smem(threads), st>>>(L.ktmp, L.iota, rs, L.n_sig_dev, shift,
+                                                          L.col_off, L.bits_y, L.skey, L.perm,
+                                                          L.parent, L.size);
         };
         if (c1) {
             p2(k_bkt_sort<true, 512, 2>, 512);
@@ -1195,7 +1219,7 @@ cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st) {
                 u32* linked = reinterpret_cast<u32*>(L.edges);  // >= 2n u32 entries
                 cudaMemsetAsync(&L.ctr->n_edges, 0, sizeof(u64), st);
                 k_bkt_cross<<<(int)std::min<u64>((nbkt + 7) / 8, (u64)L.n_sm * 8), 256, 0, st>>>(
-                    L.skey, rs, nbkt, L.col_off, cols, L.bits_y, L.parent, linked,
+                    L.skey, rs, L.n_sig_dev, shift, L.col_off, cols, L.bits_y, L.parent, linked,
                     &L.ctr->n_edges);
                 k_bkt_merge<<<L.n_sm, 256, 0, st>>>(linked, &L.ctr->n_edges, L.parent, L.size,
                                                     L.npts);

@@ -376,6 +376,8 @@ struct rg_ctx {
     bool insert_pending = false;   // KP3 in flight on aux_st (ev_kp3)
     cudaEvent_t ev_kp3 = nullptr;
     bool slot_of_valid = true;     // K2 recorded the table slots of the significant tiles
+    bool k3_speculated = false;    // the last sorted K3 ran without its sizing read (verify max_col)
+    bool k3_no_spec = false;       // redo after a failed verification: with the sizing read
     u64 order_probe[3] = {0, 0, 0};
     u64 probe_fp = 0;       // fingerprint of the probed buffer's content
     u64* k2_lb = nullptr;   // K2's look-back status words
@@ -1413,7 +1415,7 @@ rg_status prune_impl(rg_ctx* ctx, bool window_fix = false) {
 constexpr rg_status kK1Stopped = (rg_status)1000;  // internal: a deferred K1 round stopped
 
 rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused = false,
-                                  bool check_k1 = false) {
+                                  bool check_k1 = false, bool speculate = false) {
     const u64 n = fused ? n_bound : ctx->n_sig;
     const int kb = (int)(ctx->res.bits_x + ctx->res.bits_y);
     if (ctx->s_cap < n || !ctx->s_flag) {
@@ -1490,6 +1492,9 @@ rg_status agglomerate_sorted_impl(rg_ctx* ctx, u64 n_bound = ~0ull, bool fused =
     int launched = 0;
     L.launches = &launched;
     L.check_k1_stop = check_k1;
+    L.speculate = speculate && fused;
+    ctx->k3_speculated = false;
+    L.speculated = &ctx->k3_speculated;
     const cudaError_t e3 = launch_agglomerate_sorted(L, ctx->st);
     ctx->launches += launched;
     if (e3 == cudaErrorNotReady && check_k1) return kK1Stopped;
@@ -2526,8 +2531,23 @@ rg_status prune_agglomerate_fused(rg_ctx* ctx, bool window_fix) {
     CK(cudaEventRecord(ctx->ev_k3, ctx->st));
     const u64 bound = deferred ? k1_used_bound(ctx) : ctx->used;
     ctx->n_roots = ctx->n_kept = 0;
+    // K3 without its sizing read: launches sized for the bound, the exact
+    // count read on the device, the bucketed path assumed; max_col and K1's
+    // stop flag are checked in the counters read at the end of the call
+    // (RG_K3_SPEC=0: always wait for the sizing read).
+    static const bool spec_off = [] {
+        const char* v = std::getenv("RG_K3_SPEC");
+        return v && std::strcmp(v, "0") == 0;
+    }();
+    ctx->k3_speculated = false;
     if (bound) {
-        s = agglomerate_sorted_impl(ctx, bound, true, deferred);
+        // Only for small tables: with a large one the host read's bubble is
+        // where the idle table's clear (0.5 GB of writes for config 4) runs
+        // alone; without the bubble it competes with K3 (config 4: 2.46 ->
+        // 2.56 ms), while config 1 gains 5 % (0.211 -> 0.201 ms).
+        const bool small_table = ctx->cap * sizeof(Slot) <= (64ull << 20);
+        s = agglomerate_sorted_impl(ctx, bound, true, deferred,
+                                    !spec_off && !ctx->k3_no_spec && small_table);
         if (s == kK1Stopped) {
             s = k1_finish(ctx);
             if (s != RG_OK) return s;
@@ -2546,6 +2566,30 @@ rg_status prune_agglomerate_fused(rg_ctx* ctx, bool window_fix) {
     CK(cudaMemcpyAsync(ctx->hctr, ctx->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
     check_fingerprint(ctx);
+    if (ctx->k3_speculated) {
+        ctx->k3_speculated = false;
+        if (deferred && ctx->hctr->stopped) {
+            // a warp ran out of budget (the table must grow): K2/K3 ran on an
+            // incomplete table; finish K1 and run them again
+            s = k1_finish(ctx);
+            if (s != RG_OK) return s;
+            return prune_agglomerate_fused(ctx, window_fix);
+        }
+        if (ctx->hctr->max_col > sorted_bucket_max_column()) {
+            // a column too long for the bucketed sort (its blocks skipped the
+            // oversized buckets): again, with the sizing read choosing the path
+            if (deferred) {
+                ctx->used = ctx->hctr->used;
+                ctx->ingested = ctx->hctr->ingested;
+                ctx->skipped = ctx->hctr->skipped;
+                ctx->k1.active = false;
+            }
+            ctx->k3_no_spec = true;
+            s = prune_agglomerate_fused(ctx, window_fix);
+            ctx->k3_no_spec = false;
+            return s;
+        }
+    }
     if (deferred) {  // K1's counters arrive with K3's
         ctx->used = ctx->hctr->used;
         ctx->ingested = ctx->hctr->ingested;

@@ -122,7 +122,11 @@ struct SortedLaunch {
     bool check_k1_stop = false;  // the host read also checks K1's stop flag (returns
                                  // cudaErrorNotReady, nothing launched after it, if set)
     int* launches;        // out: kernels launched
+    bool speculate = false;      // no host read: size for the bound n_sig, assume the bucketed
+                                 // path; the caller verifies max_col / K1's stop flag afterwards
+    bool* speculated = nullptr;  // out: the launch really went without the host read
 };
+u64 sorted_bucket_max_column();
 size_t sorted_temp_bytes(u64 n, int bits, u32 bits_x);
 u64 sorted_columns(u32 bits_x);
 cudaError_t launch_agglomerate_sorted(const SortedLaunch& L, cudaStream_t st);
