@@ -460,8 +460,8 @@ def ours(args) -> None:
         del labels
     if not args.quick and world == 1 and args.order == "gen":
         # the same workload in a seeded random order (the reference generator
-        # shuffles, datagen.hpp:224-226): no spatial locality for K1's cache,
-        # every point reaches the HBM table
+        # shuffles, datagen.hpp:224-226): no spatial locality for K1's cache;
+        # the order probe sends it to the partitioned contraction (K1')
         g = torch.Generator(device=dev.device)
         g.manual_seed(11)
         shuf = dev[torch.randperm(n, device=dev.device, generator=g)]
@@ -477,6 +477,11 @@ def ours(args) -> None:
         torch.cuda.synchronize()
         ms_s = s0.elapsed_time(s1) / args.steps
         extra["shuffled"] = {"points_per_s": n / (ms_s / 1e3), "ms_per_step": ms_s,
+                             "roofline_frac": (BYTES_PER_POINT * n / (ms_s / 1e3))
+                             / (measured_peak_gbs()[0] * 1e9),
+                             "path": "partitioned contraction: sampled plan + one-pass scatter "
+                                     "(k_part_stream), shared-memory aggregation (k_part_agg), "
+                                     "pair inserts beside K2/K3",
                              "order": "torch.randperm(seed 11) on the device"}
         del shuf
 
