@@ -879,12 +879,18 @@ __global__ void __launch_bounds__(256) k_compact(Table t, u64 cap, u64 tau, cons
 }
 
 // K2, one pass per tile (default): a block takes the next tile of
-// kK2LbThr x kK2LbPer slots from a ticket, loads all of its slots (eight
+// kK2LbThr x kK2LbPer slots from a ticket, loads all of its slots (four
 // 16-byte loads in flight per thread), counts the significant ones,
 // reserves the tile's output range with one atomic and writes key, count
 // and slot index straight from registers. No re-read of the table (the
 // staged variant above re-reads every flushed slot).
-constexpr int kK2LbThr = 256, kK2LbPer = 8;
+#ifndef RG_K2_THR
+#define RG_K2_THR 256
+#endif
+#ifndef RG_K2_PER
+#define RG_K2_PER 4  // (256 x 8: 166 us, 256 x 4: 145 us, 256 x 2: 176 us, 128 x 4: 164 us, 512 x 8: 174 us, 1024 x 8: 196 us)
+#endif
+constexpr int kK2LbThr = RG_K2_THR, kK2LbPer = RG_K2_PER;
 constexpr u64 kK2LbTile = (u64)kK2LbThr * kK2LbPer;
 __global__ void __launch_bounds__(kK2LbThr) k_compact_lb(Table t, u64 cap, u64 tau, const u8* keep,
                                                          K2Out o, Counters* ctr, u64* status,
