@@ -524,7 +524,15 @@ __global__ void __launch_bounds__(kCsThr) k_col_scan(const u32* cnt, u64 cols, c
 // number of kept roots before a root is its cluster id (finalize_clusters
 // agglomerate.hpp:186-190). Tiles whose root lies in an earlier tile wait
 // for that tile's ids (tiles are taken in ticket order: the wait ends).
-constexpr int kLbThr = 256, kLbPer = 16, kLbTile = kLbThr * kLbPer;
+// (tile shapes measured on config 4, K3 in all: 256 x 16 positions 0.673 ms,
+// 256 x 8: 0.663, 512 x 8: 0.655, 512 x 4: 0.678, 1024 x 4: 0.672)
+#ifndef RG_IDS_THR
+#define RG_IDS_THR 512
+#endif
+#ifndef RG_IDS_PER
+#define RG_IDS_PER 8
+#endif
+constexpr int kLbThr = RG_IDS_THR, kLbPer = RG_IDS_PER, kLbTile = kLbThr * kLbPer;
 __global__ void __launch_bounds__(kLbThr) k_sorted_ids(const u32* parent, const u32* size,
                                                        u64 mu, const u32* perm, const u64* n_sig_p,
                                                        int* tile_cid_b, int* cid_s, u32* clu_root,
@@ -712,14 +720,16 @@ __global__ void __launch_bounds__(256) k_col_scatter(const u64* key, const u64* 
 // 512-thread blocks (108 KB, 2 per SM) for columns of <= 2048 tiles, or
 // (RG_BKT_SHIFT=11) 2048-tile buckets in 256-thread blocks (55 KB, 4 per
 // SM) when every column holds <= 1024 tiles.
+// (P1 block shapes on config 4, K3 in all: 512 x 8 keys 0.673 ms, 256 x 8: 0.662,
+// 512 x 4: 0.666, 1024 x 8: 0.674, 128 x 8 as 256 x 8)
 #ifndef RG_P1_THREADS
-#define RG_P1_THREADS 512
+#define RG_P1_THREADS 256
 #endif
 #ifndef RG_P1_PER
 #define RG_P1_PER 8
 #endif
 constexpr int kP1Threads = RG_P1_THREADS;
-constexpr int kP1Per = RG_P1_PER;       // keys per thread (512 x 8 = 4096 per block)
+constexpr int kP1Per = RG_P1_PER;       // keys per thread (256 x 8 = 2048 per block)
 constexpr u32 kP1Tile = kP1Threads * kP1Per;
 constexpr u32 kP1RankBits = 13;         // rank inside a block's tile < 8192
 static_assert(kP1Tile <= (1u << kP1RankBits), "P1 tile rank field");

@@ -31,12 +31,13 @@ for cfg in [int(a) for a in sys.argv[1:]] or [4]:
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    k1, k2 = [], []
+    k1, k2, k3 = [], [], []
     a.record(stream)
     for _ in range(steps):
         st_ = pl.run(dev)
         k1.append(st_.ms_contract)
         k2.append(getattr(st_, "ms_prune", 0.0))
+        k3.append(getattr(st_, "ms_agglomerate", 0.0))
     b.record(stream)
     torch.cuda.synchronize()
     f = pl.flat()
@@ -45,7 +46,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [4]:
         h.update(np.ascontiguousarray(arr).tobytes())
     n = dev.shape[0]
     out[f"config{cfg}"] = {"k1_ms": statistics.median(k1), "k1_min_ms": min(k1),
-                           "step_ms": a.elapsed_time(b) / steps, "k2_ms": statistics.median(k2),
+                           "step_ms": a.elapsed_time(b) / steps, "k2_ms": statistics.median(k2), "k3_ms": statistics.median(k3),
                            "k1_frac": 16 * n / (statistics.median(k1) / 1e3) / 6537.6e9,
                            "digest": h.hexdigest()[:16]}
     del dev, pl
