@@ -24,7 +24,13 @@ namespace rg {
 
 constexpr int kLWarps = 4;
 constexpr int kLBatch = 2;
-constexpr int kLRing = 4;     // rows in flight per warp (cp.async ring)
+#ifndef RG_K4_RING
+#define RG_K4_RING 4
+#endif
+#ifndef RG_K4_MINBLOCKS
+#define RG_K4_MINBLOCKS 12  // (config 4 labels: 8 blocks/SM 2.00 ms, 10: 2.00, 12: 1.96, 14 and 16: 2.10)
+#endif
+constexpr int kLRing = RG_K4_RING;     // rows in flight per warp (cp.async ring)
 constexpr int kLCache = 128;
 constexpr u32 kLRowsPerSeg = 256;
 
@@ -70,7 +76,7 @@ __device__ __forceinline__ int l_row(const Grid& g, const Table& t, const int* t
 // Segments of kLRowsPerSeg rows are dealt to warps round-robin; each warp
 // streams its rows through a per-lane cp.async ring like K1.
 template <bool kAligned, bool kNarrow, bool kCid>
-__global__ void __launch_bounds__(kLWarps * 32, 8) k_label_points(const double* xy, u64 n, Grid g,
+__global__ void __launch_bounds__(kLWarps * 32, RG_K4_MINBLOCKS) k_label_points(const double* xy, u64 n, Grid g,
                                                                   Table t, const int* tile_cid,
                                                                   int* labels) {
     __shared__ LSmem s_warp[kLWarps];
@@ -315,10 +321,15 @@ __device__ __forceinline__ int cell_try(u64 a0, u64 m0, u64 a1, u64 m1, u32 cell
     return (!a0 || !a1) ? -1 : 0;
 }
 
-// Lookups of kLkIlp points per thread: the point loads are in flight
-// together; each lookup reads one 32-byte bucket (2 entries) and walks on
-// only when a full bucket does not hold the cell.
-constexpr int kLkIlp = 4;
+// Lookups of kLkIlp points per thread and trip: the point loads are in
+// flight together; each lookup reads one 32-byte bucket (2 entries) and walks
+// on only when a full bucket does not hold the cell. (One point per trip is
+// fastest: the kernel is bound by random L2 sectors, and more points per
+// thread only delay the lookups behind the point loads.)
+#ifndef RG_K4P_ILP
+#define RG_K4P_ILP 1  // (config 4 random-order labels: 1 point per thread and trip 4.44 ms, 2: 4.62, 4: 4.71, 8: 6.01)
+#endif
+constexpr int kLkIlp = RG_K4P_ILP;
 __global__ void __launch_bounds__(256) k_label_cells(const double2* xy, u64 n, Grid g,
                                                      const ulonglong2* tab, u64 nb,
                                                      const int* ids, int* labels) {
