@@ -99,6 +99,18 @@ def test_points_config3_properties():
     assert bool(torch.all(le | boundary))
 
 
+def test_points_of_an_unordered_device_input():
+    """10M points of config 4 in a random order on the device: the
+    partitioned contraction with K2 on its pairs, then the point lists
+    (labels through the cell table) against the oracle + host sort."""
+    gp = D.params(4)
+    pts = D.generate(D.spec(4, 0.02), shuffle_seed=21)
+    xy, off = run_points(pts, gp, dev=True)
+    exy, eoff = expected_points(pts, gp)
+    assert np.array_equal(off, eoff)
+    assert np.array_equal(xy, exy)
+
+
 def test_points_no_clusters_and_empty():
     gp = GridParams(precision=2.0, threshold=100, min_cluster_size=1)
     xy, off = run_points(np.random.default_rng(1).normal(0, 1, size=(1000, 2)), gp)
